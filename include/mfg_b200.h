@@ -1,0 +1,168 @@
+/*
+ * mfg_b200.h — C ABI of the B200-native Omega-sweep library (libmfg_b200.so).
+ *
+ * The reference (mfglobal 0.1.0, pure Python) has no FFI of its own: its hot
+ * path bottoms out in numpy/scipy C extensions. Each entry point below
+ * replaces one of those call sites; the reference interface it stands in for
+ * is cited as mfg/<file>:<line> with mfg = /root/reference/pkg/src/mfglobal.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless the name ends in _host.
+ *  - Nothing here allocates device memory: callers size workspaces with the
+ *    *_workspace() queries and pass them in.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *    and returns an mfg_status; mfg_last_error() gives a message.
+ *  - dtype selects the storage type of Omega values and dense factors:
+ *    MFG_F32 (float) or MFG_F64 (double). Reductions are always fp64.
+ *  - Dense matrices are row-major with a leading dimension (elements).
+ *  - Omega indices are int32 (|Omega| < 2^31; checked at build time).
+ */
+#ifndef MFG_B200_H
+#define MFG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MFG_OK = 0,
+  MFG_ERR_ARG = 1,          /* shape / argument error      -> ValueError        */
+  MFG_ERR_DATASET = 2,      /* range / duplicate in Omega  -> DatasetError      */
+  MFG_ERR_CAPACITY = 3,     /* too large for int32 / ws    -> CapacityError     */
+  MFG_ERR_CUDA = 4,         /* CUDA runtime error          -> RuntimeError      */
+  MFG_ERR_NUMERICAL = 5     /* non-SPD normal matrix etc.  -> NumericalError    */
+} mfg_status;
+
+typedef enum { MFG_F32 = 0, MFG_F64 = 1 } mfg_dtype;
+
+/* One orientation of Omega (CSR over rows, or CSC = CSR of the transpose).
+ * Built by mfg_omega_build / mfg_layout_build; the scheduling metadata
+ * (batch masks, nonempty-row ranks) drives the load-balanced flat-chunk
+ * kernels, so Zipf-skewed rows need no special casing. */
+typedef struct {
+  int32_t nrows;            /* rows in this orientation                         */
+  int32_t ncols;            /* columns in this orientation                      */
+  int64_t nnz;
+  const int32_t* ptr;       /* [nrows+1]  row pointers                          */
+  const int32_t* idx;       /* [nnz]      column index of each entry            */
+  const int32_t* row_of;    /* [nnz]      row of each entry (COO)               */
+  const uint32_t* bmask;    /* [ceil(nnz/32)] bit l: entry 32b+l starts a row    */
+  const int32_t* brank;     /* [ceil(nnz/32)] nonempty-row rank of entry 32b    */
+  const int32_t* nzrows;    /* [n_nonempty] rank -> row                          */
+  int32_t n_nonempty;
+  const int32_t* empty_rows;/* [n_empty]  rows without entries                   */
+  int32_t n_empty;
+} mfg_layout;
+
+const char* mfg_last_error(void);
+int mfg_version(void);
+/* number of kernel launches issued by this library since load (diagnostics) */
+int64_t mfg_launch_count(void);
+
+/* ---- Omega build ------------------------------------------------------
+ * Replaces ObservationSet.from_coo (mfg/data.py:70-102): range checks,
+ * (row, col) lexicographic sort, duplicate rejection, CSR row pointers; and
+ * the CSC view a_csr_t = a_csr.T.tocsr() (mfg/data.py:113-119, 156-158).
+ * Inputs are int64 COO (as the reference stores them) and fp64 values.
+ * Outputs (all device): CSR (rows_out/cols_out/vals_out in (row,col) order,
+ * ptr), CSC (csc_ptr, csc_rows, csc_perm = CSR position of each CSC entry).
+ * On duplicates returns MFG_ERR_DATASET and writes the first duplicate's
+ * sorted position to *dup_pos_host (-1 otherwise; host pointer).          */
+size_t mfg_omega_build_workspace(int64_t nnz, int32_t m, int32_t n);
+int mfg_omega_build(int32_t m, int32_t n, int64_t nnz,
+                    const int64_t* rows_in, const int64_t* cols_in,
+                    const double* vals_in,
+                    int32_t* rows_out, int32_t* cols_out, double* vals_out,
+                    int32_t* ptr, int32_t* csc_ptr, int32_t* csc_rows,
+                    int32_t* csc_cols, int32_t* csc_perm,
+                    int64_t* dup_pos_host, int32_t* range_err_host,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* Scheduling metadata for one orientation, from its ptr/row_of arrays.
+ * bmask/brank sized ceil(nnz/32); nzrows sized nrows; empty_rows sized nrows.
+ * Writes counts to the host ints.                                          */
+size_t mfg_layout_workspace(int64_t nnz, int32_t nrows);
+int mfg_layout_build(int32_t nrows, int64_t nnz, const int32_t* ptr,
+                     const int32_t* row_of, uint32_t* bmask, int32_t* brank,
+                     int32_t* nzrows, int32_t* empty_rows,
+                     int32_t* n_nonempty_host, int32_t* n_empty_host,
+                     void* workspace, size_t ws_bytes, void* stream);
+
+/* Gather: out[e] = src[perm[e]] (values into the CSC order).               */
+int mfg_gather(int dtype, int64_t nnz, const int32_t* perm, const void* src,
+               void* out, void* stream);
+/* dtype conversion of a flat array (f64 <-> f32)                           */
+int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src,
+                void* out, void* stream);
+
+/* ---- The Omega sweep (the metric's unit of work) ----------------------
+ * One launch pair computing, for fixed W (m x k) and H (n x k):
+ *   R = P_Omega(W H^T) - A            (SDDMM; pair_values/residual_on_omega,
+ *                                      mfg/data.py:253-280)
+ *   RH  = R . H     (m x k)           (CSR SpMM, mfg/operators.py:108 /
+ *                                      mfg/mfsolver.py:74)
+ *   RtW = R^T . W   (n x k)           (CSC SpMM, mfg/operators.py:117)
+ *   sums[0] = sum r^2 (loss_quad, mfg/data.py:291-293),
+ *   sums[1] = ||W||_F^2, sums[2] = ||H||_F^2 (FactorPair.frob_sq,
+ *                                      mfg/operators.py:53-55).
+ * Both orientations are processed in the same launch (the CSC pass
+ * recomputes r from its own value copy instead of gathering R).
+ * Any of R/RH/RtW may be NULL to skip that output. out_scale multiplies
+ * RH and RtW (e.g. 2 for gradients). vals_csc is A in CSC order.
+ * compute_f64 != 0 forces fp64 arithmetic on f32 storage.                 */
+size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);
+int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr,
+              const mfg_layout* csc, int k, const void* vals_csr,
+              const void* vals_csc, const void* W, int ldw, const void* H,
+              int ldh, void* R, void* RH, void* RtW, double out_scale,
+              double* sums, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- SDDMM with fused reductions --------------------------------------
+ * p_e = sum_d L[row_e, d] * (scale ? scale[d] : 1) * Rt[col_e, d]
+ * r_e = p_e - A_e (A may be NULL -> 0)
+ * out_e = out_mult * r_e (out may be NULL)
+ * sums[0] += sum r_e^2;   if G: sums[1] += sum G_e (r_e - G_e/2);
+ * sums[2] += sum G_e p_e   (all fp64; sums must hold 3 doubles)
+ * Covers residual_on_omega(_svd) (mfg/data.py:272-288), triplet_values
+ * (266-269), the Eq.5 terms f_next / g_inner (mfg/proxlift.py:374-377) and
+ * ShiftedOperator.frob_sq's x_Omega.g (mfg/operators.py:142-152).         */
+size_t mfg_sddmm_workspace(const mfg_layout* lay, int k);
+int mfg_sddmm(int dtype, int compute_f64, const mfg_layout* lay, int k,
+              const void* L, int ldl, const double* scale, const void* Rt,
+              int ldr, const void* A, const void* G, double out_mult,
+              void* out, double* sums, void* workspace, size_t ws_bytes,
+              void* stream);
+
+/* ---- SpMM over Omega --------------------------------------------------
+ * Y = alpha * S X + beta * Y, S the sparse matrix with values `vals` in the
+ * layout's order (CSR: grad.csr @ block, mfg/operators.py:108; pass the CSC
+ * layout and CSC-ordered values for grad.csr_t @ block, 117/135).
+ * X is (ncols x p), Y is (nrows x p).                                     */
+size_t mfg_spmm_workspace(const mfg_layout* lay, int p);
+int mfg_spmm(int dtype, const mfg_layout* lay, int p, const void* vals,
+             const void* X, int ldx, double alpha, double beta, void* Y,
+             int ldy, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- BCD half-sweep ---------------------------------------------------
+ * Exact row minimisers (mfg/mfsolver.py:53-75):
+ *   (lam I + 2 sum_{j in Omega_i} o_j o_j^T) w_i = 2 sum_j A_ij o_j
+ * Gram assembly and a per-row Cholesky solve, fp64 arithmetic for either
+ * storage type. OUT is (nrows x k).                                       */
+size_t mfg_bcd_workspace(const mfg_layout* lay, int k);
+int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k,
+                       const void* vals, const void* other, int ldo,
+                       double lam, void* out, int ldout, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/* ---- dense reductions ---------------------------------------------------
+ * sums_host-free fp64 dot: out[0] = sum_i x_i y_i over `count` entries.    */
+int mfg_dot(int dtype, int64_t count, const void* x, const void* y,
+            double* out, void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFG_B200_H */

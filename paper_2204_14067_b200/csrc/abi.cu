@@ -1,0 +1,175 @@
+// extern "C" entry points of libmfg_b200.so (see include/mfg_b200.h).
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "engine.cuh"
+
+namespace mfg {
+
+namespace {
+thread_local std::string g_err;
+
+template <typename TO, typename TI>
+__global__ void k_convert(int64_t n, const TI* __restrict__ in, TO* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (TO)in[i];
+}
+
+template <typename T>
+__global__ void k_gather(int64_t n, const int32_t* __restrict__ perm, const T* __restrict__ src,
+                         T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[perm[i]];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_dot(int64_t n, const T* __restrict__ x, const T* __restrict__ y, double* __restrict__ bp,
+      unsigned int* __restrict__ counter, double* __restrict__ out) {
+  __shared__ double sm[8];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v += (double)x[i] * (double)y[i];
+  const double s = block_sum<256>(v, sm);
+  if (threadIdx.x == 0) bp[blockIdx.x] = s;
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* b = bp;
+    double t = 0.0;
+    for (unsigned int i = 0; i < gridDim.x; ++i) t += b[i];
+    *out = t;
+    *counter = 0u;
+  }
+}
+
+inline int grid1(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > kNumSMs * 16) g = kNumSMs * 16;
+  return (int)g;
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace mfg
+
+using namespace mfg;
+
+extern "C" const char* mfg_last_error(void) { return g_err.c_str(); }
+extern "C" int mfg_version(void) { return 100; }
+extern "C" int64_t mfg_launch_count(void) { return g_launches.load(); }
+
+extern "C" int mfg_gather(int dtype, int64_t nnz, const int32_t* perm, const void* src, void* out,
+                          void* stream) {
+  if (nnz == 0) return MFG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == MFG_F64)
+    k_gather<double><<<grid1(nnz), 256, 0, s>>>(nnz, perm, (const double*)src, (double*)out);
+  else
+    k_gather<float><<<grid1(nnz), 256, 0, s>>>(nnz, perm, (const float*)src, (float*)out);
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}
+
+extern "C" int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src, void* out,
+                           void* stream) {
+  if (count == 0) return MFG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype_out == MFG_F32 && dtype_in == MFG_F64)
+    k_convert<float, double><<<grid1(count), 256, 0, s>>>(count, (const double*)src, (float*)out);
+  else if (dtype_out == MFG_F64 && dtype_in == MFG_F32)
+    k_convert<double, float><<<grid1(count), 256, 0, s>>>(count, (const float*)src, (double*)out);
+  else if (dtype_out == MFG_F64)
+    k_convert<double, double><<<grid1(count), 256, 0, s>>>(count, (const double*)src, (double*)out);
+  else
+    k_convert<float, float><<<grid1(count), 256, 0, s>>>(count, (const float*)src, (float*)out);
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}
+
+extern "C" size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
+  return sweep_workspace(csr, csc, k);
+}
+
+extern "C" int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr, const mfg_layout* csc,
+                         int k, const void* vals_csr, const void* vals_csc, const void* W, int ldw,
+                         const void* H, int ldh, void* R, void* RH, void* RtW, double out_scale,
+                         double* sums, void* workspace, size_t ws_bytes, void* stream) {
+  MFG_REQUIRE(csr && csc, "null layout");
+  MFG_REQUIRE(k >= 1, "k must be >= 1");
+  MFG_REQUIRE(csr->nrows == csc->ncols && csr->ncols == csc->nrows && csr->nnz == csc->nnz,
+              "CSR/CSC layouts disagree");
+  return sweep_dispatch(dtype, compute_f64, csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R,
+                        RH, RtW, out_scale, sums, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" size_t mfg_sddmm_workspace(const mfg_layout* lay, int k) {
+  return sddmm_workspace(lay, k);
+}
+
+extern "C" int mfg_sddmm(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,
+                         int ldl, const double* scale, const void* Rt, int ldr, const void* A,
+                         const void* G, double out_mult, void* out, double* sums, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  MFG_REQUIRE(lay, "null layout");
+  MFG_REQUIRE(k >= 0, "k must be >= 0");
+  if (k == 0) {
+    // p = 0: r = -A
+    k = 0;
+  }
+  return sddmm_dispatch(dtype, compute_f64, lay, k, L, ldl, scale, Rt, ldr, A, G, out_mult, out,
+                        sums, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" size_t mfg_spmm_workspace(const mfg_layout* lay, int p) {
+  return spmm_workspace(lay, p);
+}
+
+extern "C" int mfg_spmm(int dtype, const mfg_layout* lay, int p, const void* vals, const void* X,
+                        int ldx, double alpha, double beta, void* Y, int ldy, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  MFG_REQUIRE(lay, "null layout");
+  MFG_REQUIRE(p >= 0, "p must be >= 0");
+  return spmm_dispatch(dtype, lay, p, vals, X, ldx, alpha, beta, Y, ldy, workspace, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+extern "C" size_t mfg_bcd_workspace(const mfg_layout* lay, int k) {
+  return bcd_workspace(lay, k);
+}
+
+extern "C" int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k, const void* vals,
+                                  const void* other, int ldo, double lam, void* out, int ldout,
+                                  void* workspace, size_t ws_bytes, void* stream) {
+  MFG_REQUIRE(lay, "null layout");
+  MFG_REQUIRE(lam > 0.0, "lam must be positive");
+  return bcd_dispatch(dtype, lay, k, vals, other, ldo, lam, out, ldout, workspace, ws_bytes,
+                      (cudaStream_t)stream);
+}
+
+extern "C" int mfg_dot(int dtype, int64_t count, const void* x, const void* y, double* out,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver c(workspace, ws_bytes);
+  const int g = grid1(count);
+  double* bp = c.take<double>(g);
+  unsigned int* counter = c.take<unsigned int>(1);
+  MFG_REQUIRE(c.ok, "dot workspace too small (needs 64 KiB)");
+  MFG_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), s));
+  if (dtype == MFG_F64)
+    k_dot<double><<<g, 256, 0, s>>>(count, (const double*)x, (const double*)y, bp, counter, out);
+  else
+    k_dot<float><<<g, 256, 0, s>>>(count, (const float*)x, (const float*)y, bp, counter, out);
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}

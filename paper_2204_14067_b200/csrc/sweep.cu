@@ -1,0 +1,611 @@
+// The Omega sweep: fused SDDMM + SpMM over one or both orientations of Omega.
+//
+// Work decomposition ("flat chunks"): the nnz stream of a layout is cut into
+// chunks of `cb` 32-entry batches; one warp owns one chunk, regardless of row
+// boundaries, so Zipf-skewed degree distributions are load-balanced by
+// construction. Rows that cross a chunk boundary emit partial sums into two
+// carry slots per chunk; a deterministic epilogue adds the carries of each
+// row in chunk order, zero-fills empty rows, and reduces the per-warp fp64
+// partial sums in a fixed order. No floating-point atomics anywhere, so the
+// results are bitwise reproducible run to run.
+//
+// Per 32-entry batch (lanes over the k factor dimensions, d = lane + 32 s):
+//   1. lane t loads (col_t, A_t) coalesced; cols are broadcast through smem;
+//   2. for every slot t the warp gathers the *whole* factor row other[col_t]
+//      with one coalesced 128-byte access per 32 dimensions (the L1-wavefront
+//      optimal way to gather rows), keeping all 32 rows in registers;
+//   3. lane-partials p_t = <self_row(t), other[col_t]> restricted to the
+//      lane's dimensions; a butterfly transpose-reduction (31 shuffles for 32
+//      entries) leaves dot_t in lane t; r_t = dot_t - A_t is stored coalesced;
+//   4. the SpMM accumulation acc += r_t * other[col_t] reuses the registers of
+//      step 2, and is flushed (coalesced k-vector store) at each row change.
+// This replaces pair_values (mfg/data.py:253-263, an einsum over gathered
+// rows) and scipy csr_matvecs (grad.csr @ block, mfg/operators.py:108,117).
+#include "common.cuh"
+#include "engine.cuh"
+
+namespace mfg {
+
+std::atomic<int64_t> g_launches{0};
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerBlock = kThreads / 32;
+
+// Fixed-pattern butterfly: lane l ends with sum over lanes of v[l].
+template <typename T>
+__device__ __forceinline__ T transpose_reduce(T (&v)[32]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const T send = upper ? v[i] : v[i + s];
+      const T keep = upper ? v[i + s] : v[i];
+      v[i] = keep + shfl_xor(send, s);
+    }
+  }
+  return v[0];
+}
+
+template <typename TS, typename TC>
+struct Pass {
+  mfg_layout lay;
+  const TS* vals;       // A (may be null -> 0)
+  const TS* G;          // optional gradient values (SDDMM reductions)
+  const TS* self;       // row factor
+  int lds;
+  const double* scale;  // optional per-dim scale of self
+  const TS* other;      // gathered factor
+  int ldo;
+  TS* R;                // optional residual output (layout order)
+  double r_mult;        // R = r_mult * r
+  TS* out;              // optional SpMM output (nrows x k)
+  int ldout;
+  double out_scale;
+  int cb;               // batches per chunk
+  int nchunks;
+  TC* carry_vec;        // [2*nchunks][k]
+  int32_t* carry_row;   // [2*nchunks]
+  double* part;         // [3][nchunks] per-warp partial sums (or null)
+  int want_sq;          // accumulate sum r^2 into part[0]
+};
+
+template <typename TS, typename TC>
+__device__ __forceinline__ TC ld_self(const Pass<TS, TC>& P, int row, int d, int k) {
+  if (d >= k) return TC(0);
+  TC v = (TC)P.self[(int64_t)row * P.lds + d];
+  if (P.scale) v *= (TC)P.scale[d];
+  return v;
+}
+
+// Process one chunk. S = dimension slices held in registers (k <= 32*S when
+// !MULTI; with MULTI, k is processed in 32*S-wide dimension chunks, the
+// accumulator lives in shared memory across batches and the gathered rows are
+// re-read (L1/L2-resident) for the accumulation).
+template <typename TS, typename TC, int S, bool ACC, bool MULTI>
+__device__ void run_chunk(const Pass<TS, TC>& P, int chunk, int k, int32_t* s_col,
+                          TC* s_r, TC* s_acc) {
+  const int lane = lane_id();
+  const int64_t nnz = P.lay.nnz;
+  const int64_t E0 = (int64_t)chunk * P.cb * 32;
+  if (E0 >= nnz) return;
+  const int64_t E1 = min(E0 + (int64_t)P.cb * 32, nnz);
+  const int nkc = MULTI ? (k + 32 * S - 1) / (32 * S) : 1;
+  const int64_t b0 = E0 / 32;
+  const bool start_cross = (P.lay.bmask[b0] & 1u) == 0u;
+  const bool end_cross = (E1 < nnz) && ((P.lay.bmask[E1 / 32] & 1u) == 0u);
+
+  int rank = P.lay.brank[b0];
+  int row = P.lay.nzrows[rank];
+  bool first_row = true;
+  bool used_first = false, used_last = false;
+  int row_first = -1, row_last = -1;
+
+  TC acc[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) acc[s] = TC(0);
+  if (MULTI && ACC) {
+    for (int d = lane; d < k; d += 32) s_acc[d] = TC(0);
+  }
+  double sq = 0.0, s1 = 0.0, s2 = 0.0;
+
+  // flush the accumulated vector of `frow` (dims slice kc)
+  auto flush = [&](int frow, bool is_first, bool is_last, int kc) {
+    const bool cross_start = is_first && start_cross;
+    const bool cross_end = is_last && end_cross;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int d = kc * 32 * S + lane + 32 * s;
+      if (d < k) {
+        const TC v = MULTI ? s_acc[d] : acc[s];
+        if (cross_start) {
+          P.carry_vec[(int64_t)(2 * chunk) * k + d] = v;
+        } else if (cross_end) {
+          P.carry_vec[(int64_t)(2 * chunk + 1) * k + d] = v;
+        } else {
+          P.out[(int64_t)frow * P.ldout + d] = (TS)(v * (TC)P.out_scale);
+        }
+      }
+    }
+    if (cross_start) { used_first = true; row_first = frow; }
+    else if (cross_end) { used_last = true; row_last = frow; }
+  };
+
+  const int nb = (int)((E1 - E0 + 31) / 32);
+  for (int bi = 0; bi < nb; ++bi) {
+    const int64_t Eb = E0 + (int64_t)bi * 32;
+    const int nvalid = (int)min((int64_t)32, E1 - Eb);
+    const int64_t e = Eb + lane;
+    const bool valid = lane < nvalid;
+    const uint32_t mask = P.lay.bmask[Eb / 32] & (bi == 0 ? ~1u : ~0u);
+    int col = 0;
+    TC a = TC(0), gval = TC(0);
+    if (valid) {
+      col = P.lay.idx[e];
+      if (P.vals) a = (TC)P.vals[e];
+      if (P.G) gval = (TC)P.G[e];
+    }
+    __syncwarp();
+    s_col[lane] = col;
+    __syncwarp();
+
+    const int rank_b = rank, row_b = row;  // state at batch start (for loop 2)
+    TC p[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) p[t] = TC(0);
+    TS h[32][S];
+
+    for (int kc = 0; kc < nkc; ++kc) {
+      // issue all gathers for this dimension chunk
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int j = s_col[t];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const int d = kc * 32 * S + lane + 32 * s;
+          h[t][s] = (t < nvalid && d < k) ? P.other[(int64_t)j * P.ldo + d] : TS(0);
+        }
+      }
+      // lane partial dot products, reloading self at row changes
+      int rk = rank_b, rw = row_b;
+      TC w[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) w[s] = ld_self(P, rw, kc * 32 * S + lane + 32 * s, k);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if (t < nvalid) {
+          if ((mask >> t) & 1u) {
+            ++rk;
+            rw = P.lay.nzrows[rk];
+#pragma unroll
+            for (int s = 0; s < S; ++s) w[s] = ld_self(P, rw, kc * 32 * S + lane + 32 * s, k);
+          }
+#pragma unroll
+          for (int s = 0; s < S; ++s) p[t] += w[s] * (TC)h[t][s];
+        }
+      }
+    }
+    const TC dot = transpose_reduce(p);
+    const TC r = valid ? dot - a : TC(0);
+    if (valid) {
+      if (P.R) P.R[e] = (TS)(r * (TC)P.r_mult);
+      if (P.want_sq) sq += (double)r * (double)r;
+      if (P.G) {
+        s1 += (double)gval * ((double)r - 0.5 * (double)gval);
+        s2 += (double)gval * (double)dot;
+      }
+    }
+
+    if (ACC && P.out) {
+      __syncwarp();
+      s_r[lane] = r;
+      __syncwarp();
+      for (int kc = 0; kc < nkc; ++kc) {
+        if (MULTI) {
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const int d = kc * 32 * S + lane + 32 * s;
+            acc[s] = d < k ? s_acc[d] : TC(0);
+          }
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int j = s_col[t];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              const int d = kc * 32 * S + lane + 32 * s;
+              h[t][s] = (t < nvalid && d < k) ? P.other[(int64_t)j * P.ldo + d] : TS(0);
+            }
+          }
+        }
+        int rk = rank_b, rw = row_b;
+        bool fr = first_row;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          if (t < nvalid) {
+            if ((mask >> t) & 1u) {
+              if (MULTI) {
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                  const int d = kc * 32 * S + lane + 32 * s;
+                  if (d < k) s_acc[d] = acc[s];
+                }
+              }
+              flush(rw, fr, false, kc);
+              fr = false;
+              ++rk;
+              rw = P.lay.nzrows[rk];
+#pragma unroll
+              for (int s = 0; s < S; ++s) acc[s] = TC(0);
+            }
+            const TC rt = s_r[t];
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] += rt * (TC)h[t][s];
+          }
+        }
+        if (MULTI) {
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const int d = kc * 32 * S + lane + 32 * s;
+            if (d < k) s_acc[d] = acc[s];
+          }
+        }
+        if (kc == nkc - 1) {
+          rank = rk;
+          row = rw;
+          first_row = fr;
+        }
+      }
+    } else {
+      // advance row state without accumulation (uniform across the warp)
+      rank += __popc(mask & (nvalid == 32 ? 0xffffffffu : ((1u << nvalid) - 1u)));
+      row = P.lay.nzrows[rank];
+      first_row = false;
+    }
+  }
+  if (ACC && P.out) {
+    // final row of the chunk
+    for (int kc = 0; kc < nkc; ++kc) flush(row, first_row, true, kc);
+    if (lane == 0) {
+      P.carry_row[2 * chunk] = used_first ? row_first : -1;
+      P.carry_row[2 * chunk + 1] = used_last ? row_last : -1;
+    }
+  }
+  if (P.part) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      P.part[chunk] = sq;
+      P.part[P.nchunks + chunk] = s1;
+      P.part[2 * P.nchunks + chunk] = s2;
+    }
+  }
+}
+
+template <typename TS, typename TC, int S, bool ACC, bool MULTI>
+__global__ void __launch_bounds__(kThreads)
+k_sweep(Pass<TS, TC> P0, Pass<TS, TC> P1, int nw0, int nw_total, int k) {
+  __shared__ int32_t s_col[kWarpsPerBlock][32];
+  __shared__ TC s_r[kWarpsPerBlock][32];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int wib = threadIdx.x >> 5;
+  TC* s_acc = MULTI ? reinterpret_cast<TC*>(s_dyn) + (size_t)wib * k : nullptr;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  if (gw >= nw_total) return;
+  if (gw < nw0) run_chunk<TS, TC, S, ACC, MULTI>(P0, gw, k, s_col[wib], s_r[wib], s_acc);
+  else run_chunk<TS, TC, S, ACC, MULTI>(P1, gw - nw0, k, s_col[wib], s_r[wib], s_acc);
+}
+
+// Epilogue: carries, empty rows, deterministic reductions.
+struct SumJob {
+  const double* part;  // [3][np]
+  int np;
+  const void* W;       // optional dense norms
+  int64_t wcount;
+  const void* H;
+  int64_t hcount;
+  int is_f64;
+  double* block_part;  // [gridDim.x][5]
+  unsigned int* counter;
+  double* sums;        // [5] out: sq, s1, s2, |W|^2, |H|^2 (first 3 used by callers)
+};
+
+template <typename TS, typename TC>
+__device__ void carry_fixup(const Pass<TS, TC>& P, int k, int warp_global, int nwarps_grid) {
+  const int lane = lane_id();
+  const int nslots = 2 * P.nchunks;
+  for (int q = 2 * warp_global + 1; q < nslots; q += 2 * nwarps_grid) {
+    const int row = P.carry_row[q];
+    if (row < 0) continue;
+    for (int d0 = 0; d0 < k; d0 += 32) {
+      const int d = d0 + lane;
+      TC v = TC(0);
+      if (d < k) v = P.carry_vec[(int64_t)q * k + d];
+      for (int nx = q + 1; nx < nslots; ++nx) {
+        const int r2 = P.carry_row[nx];
+        if (r2 < 0) continue;
+        if (r2 != row) break;
+        if (d < k) v += P.carry_vec[(int64_t)nx * k + d];
+      }
+      if (d < k) P.out[(int64_t)row * P.ldout + d] = (TS)(v * (TC)P.out_scale);
+    }
+  }
+  // rows whose only contribution came through a start-crossing slot cannot
+  // occur: a start crossing implies the previous chunk's end crossing (an odd
+  // head slot) or a single-row previous chunk whose run began earlier.
+  for (int i = warp_global; i < P.lay.n_empty; i += nwarps_grid) {
+    const int row2 = P.lay.empty_rows[i];
+    for (int d = lane; d < k; d += 32) P.out[(int64_t)row2 * P.ldout + d] = TS(0);
+  }
+}
+
+__device__ __forceinline__ double ldv(const void* p, int64_t i, int is_f64) {
+  return is_f64 ? static_cast<const double*>(p)[i] : (double)static_cast<const float*>(p)[i];
+}
+
+template <typename TS, typename TC>
+__global__ void __launch_bounds__(256)
+k_epilogue(Pass<TS, TC> P0, int has0, Pass<TS, TC> P1, int has1, int k, SumJob J) {
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwg = (gridDim.x * blockDim.x) >> 5;
+  if (has0 && P0.out) carry_fixup(P0, k, wg, nwg);
+  if (has1 && P1.out) carry_fixup(P1, k, wg, nwg);
+  if (!J.block_part) return;
+  // per-block partials over fixed slices
+  __shared__ double sm[8];
+  double v[5] = {0, 0, 0, 0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < J.np; i += gridDim.x * blockDim.x) {
+    v[0] += J.part[i];
+    v[1] += J.part[J.np + i];
+    v[2] += J.part[2 * J.np + i];
+  }
+  if (J.W)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < J.wcount;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const double x = ldv(J.W, i, J.is_f64);
+      v[3] += x * x;
+    }
+  if (J.H)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < J.hcount;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const double x = ldv(J.H, i, J.is_f64);
+      v[4] += x * x;
+    }
+  for (int c = 0; c < 5; ++c) {
+    const double s = block_sum<256>(v[c], sm);
+    if (threadIdx.x == 0) J.block_part[blockIdx.x * 5 + c] = s;
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int done = atomicAdd(J.counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 5) {
+    __threadfence();
+    double s = 0.0;
+    const volatile double* bp = J.block_part;
+    for (unsigned int b = 0; b < gridDim.x; ++b) s += bp[b * 5 + threadIdx.x];
+    J.sums[threadIdx.x] = s;
+    if (threadIdx.x == 0) *J.counter = 0u;
+  }
+}
+
+constexpr int kEpiBlocks = 2 * kNumSMs;
+
+int pick_cb(int64_t nnz) {
+  // target >= ~16 warps per SM of chunks, batches in [2, 32]
+  int64_t target_chunks = (int64_t)kNumSMs * 16;
+  int64_t cb = (nnz / 32 + target_chunks - 1) / target_chunks;
+  if (cb < 2) cb = 2;
+  if (cb > 32) cb = 32;
+  return (int)cb;
+}
+
+int chunks_of(int64_t nnz, int cb) {
+  return (int)((nnz + (int64_t)cb * 32 - 1) / ((int64_t)cb * 32));
+}
+
+template <typename C>
+void carve_pass(C& c, const mfg_layout* lay, int k, bool acc, bool part) {
+  if (!lay) return;
+  const int cb = pick_cb(lay->nnz);
+  const int nch = chunks_of(lay->nnz, cb) > 0 ? chunks_of(lay->nnz, cb) : 1;
+  if (acc) {
+    c.template take<double>((size_t)2 * nch * k);  // carry vecs (sized for fp64)
+    c.template take<int32_t>((size_t)2 * nch);
+  }
+  if (part) c.template take<double>((size_t)3 * nch);
+}
+
+template <typename C>
+void carve_epi(C& c) {
+  c.template take<double>((size_t)kEpiBlocks * 5);
+  c.template take<unsigned int>(1);
+  c.template take<double>(5);
+}
+
+template <typename TS, typename TC>
+bool setup_pass(Pass<TS, TC>& P, Carver& c, const mfg_layout* lay, int k, bool acc, bool part) {
+  P.lay = *lay;
+  P.cb = pick_cb(lay->nnz);
+  P.nchunks = chunks_of(lay->nnz, P.cb);
+  const int nch = P.nchunks > 0 ? P.nchunks : 1;
+  P.carry_vec = nullptr;
+  P.carry_row = nullptr;
+  P.part = nullptr;
+  if (acc) {
+    P.carry_vec = reinterpret_cast<TC*>(c.take<double>((size_t)2 * nch * k));
+    P.carry_row = c.take<int32_t>((size_t)2 * nch);
+  }
+  if (part) P.part = c.take<double>((size_t)3 * nch);
+  return c.ok;
+}
+
+template <typename TS, typename TC, bool ACC>
+int launch_main(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int n0, int n1, int k,
+                cudaStream_t stream) {
+  const int nwt = n0 + n1;
+  if (nwt == 0) return MFG_OK;
+  const int grid = (nwt + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const bool f32s = sizeof(TS) == 4;
+  if (k <= 32) {
+    k_sweep<TS, TC, 1, ACC, false><<<grid, kThreads, 0, stream>>>(P0, P1, n0, nwt, k);
+  } else if (k <= 64 && f32s) {
+    k_sweep<TS, TC, 2, ACC, false><<<grid, kThreads, 0, stream>>>(P0, P1, n0, nwt, k);
+  } else {
+    const size_t smem = ACC ? (size_t)kWarpsPerBlock * k * sizeof(TC) : 0;
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(k_sweep<TS, TC, 1, ACC, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    k_sweep<TS, TC, 1, ACC, true><<<grid, kThreads, smem, stream>>>(P0, P1, n0, nwt, k);
+  }
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}
+
+template <typename TS, typename TC>
+int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* vals_csr,
+             const void* vals_csc, const void* W, int ldw, const void* H, int ldh, void* R,
+             void* RH, void* RtW, double out_scale, double* sums, void* ws, size_t wsb,
+             cudaStream_t stream) {
+  Carver c(ws, wsb);
+  Pass<TS, TC> P0{}, P1{};
+  const bool acc0 = RH != nullptr, acc1 = RtW != nullptr;
+  if (!setup_pass(P0, c, csr, k, acc0, true)) goto small;
+  if (!setup_pass(P1, c, csc, k, acc1, false)) goto small;
+  {
+    P0.vals = (const TS*)vals_csr; P0.G = nullptr; P0.self = (const TS*)W; P0.lds = ldw;
+    P0.scale = nullptr; P0.other = (const TS*)H; P0.ldo = ldh; P0.R = (TS*)R; P0.r_mult = 1.0;
+    P0.out = (TS*)RH; P0.ldout = k; P0.out_scale = out_scale; P0.want_sq = 1;
+    P1.vals = (const TS*)vals_csc; P1.G = nullptr; P1.self = (const TS*)H; P1.lds = ldh;
+    P1.scale = nullptr; P1.other = (const TS*)W; P1.ldo = ldw; P1.R = nullptr; P1.r_mult = 1.0;
+    P1.out = (TS*)RtW; P1.ldout = k; P1.out_scale = out_scale; P1.want_sq = 0;
+    SumJob J{};
+    J.block_part = c.take<double>((size_t)kEpiBlocks * 5);
+    J.counter = c.take<unsigned int>(1);
+    double* tmp = c.take<double>(5);
+    if (!c.ok) goto small;
+    J.part = P0.part; J.np = P0.nchunks;
+    J.W = W; J.wcount = (ldw == k) ? (int64_t)csr->nrows * k : 0;
+    J.H = H; J.hcount = (ldh == k) ? (int64_t)csc->nrows * k : 0;
+    J.is_f64 = sizeof(TS) == 8;
+    J.sums = tmp;
+    if (ldw != k || ldh != k) { set_error("sweep requires ldw == ldh == k"); return MFG_ERR_ARG; }
+    // counter must start at zero: the epilogue's last block re-zeroes it.
+    MFG_CUDA_CHECK(cudaMemsetAsync(J.counter, 0, sizeof(unsigned int), stream));
+    const int n0 = csr->nnz ? P0.nchunks : 0;
+    const int n1 = (acc1 && csc->nnz) ? P1.nchunks : 0;
+    int st;
+    if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
+    else st = launch_main<TS, TC, false>(P0, P1, n0, 0, k, stream);
+    if (st != MFG_OK) return st;
+    if (n0 == 0) {  // no entries: partials are zero
+      MFG_CUDA_CHECK(cudaMemsetAsync(P0.part, 0, sizeof(double) * 3, stream));
+      J.np = 1;
+    }
+    k_epilogue<TS, TC><<<kEpiBlocks, 256, 0, stream>>>(P0, acc0 ? 1 : 0, P1, acc1 ? 1 : 0, k, J);
+    MFG_LAUNCH_CHECK();
+    // sums = [sq, |W|^2, |H|^2]
+    MFG_CUDA_CHECK(cudaMemcpyAsync(sums, tmp, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    MFG_CUDA_CHECK(cudaMemcpyAsync(sums + 1, tmp + 3, 2 * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, stream));
+    return MFG_OK;
+  }
+small:
+  set_error("sweep workspace too small");
+  return MFG_ERR_ARG;
+}
+
+template <typename TS, typename TC>
+int do_sddmm(const mfg_layout* lay, int k, const void* L, int ldl, const double* scale,
+             const void* Rt, int ldr, const void* A, const void* G, double out_mult, void* out,
+             double* sums, void* ws, size_t wsb, cudaStream_t stream) {
+  Carver c(ws, wsb);
+  Pass<TS, TC> P{};
+  if (!setup_pass(P, c, lay, k, false, true)) {
+    set_error("sddmm workspace too small");
+    return MFG_ERR_ARG;
+  }
+  P.vals = (const TS*)A; P.G = (const TS*)G; P.self = (const TS*)L; P.lds = ldl; P.scale = scale;
+  P.other = (const TS*)Rt; P.ldo = ldr; P.R = (TS*)out; P.r_mult = out_mult; P.out = nullptr;
+  P.ldout = 0; P.out_scale = 1.0; P.want_sq = 1;
+  SumJob J{};
+  J.block_part = c.take<double>((size_t)kEpiBlocks * 5);
+  J.counter = c.take<unsigned int>(1);
+  double* tmp = c.take<double>(5);
+  if (!c.ok) {
+    set_error("sddmm workspace too small");
+    return MFG_ERR_ARG;
+  }
+  J.part = P.part; J.np = P.nchunks; J.is_f64 = sizeof(TS) == 8; J.sums = tmp;
+  MFG_CUDA_CHECK(cudaMemsetAsync(J.counter, 0, sizeof(unsigned int), stream));
+  const int n0 = lay->nnz ? P.nchunks : 0;
+  int st = launch_main<TS, TC, false>(P, P, n0, 0, k, stream);
+  if (st != MFG_OK) return st;
+  if (n0 == 0) {
+    MFG_CUDA_CHECK(cudaMemsetAsync(P.part, 0, sizeof(double) * 3, stream));
+    J.np = 1;
+  }
+  k_epilogue<TS, TC><<<kEpiBlocks, 256, 0, stream>>>(P, 0, P, 0, k, J);
+  MFG_LAUNCH_CHECK();
+  if (sums)
+    MFG_CUDA_CHECK(cudaMemcpyAsync(sums, tmp, 3 * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  return MFG_OK;
+}
+
+}  // namespace
+
+size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
+  Sizer s;
+  carve_pass(s, csr, k, true, true);
+  carve_pass(s, csc, k, true, false);
+  carve_epi(s);
+  return s.off + 1024;
+}
+
+size_t sddmm_workspace(const mfg_layout* lay, int k) {
+  Sizer s;
+  carve_pass(s, lay, k, false, true);
+  carve_epi(s);
+  return s.off + 1024;
+}
+
+int sweep_dispatch(int dtype, int compute_f64, const mfg_layout* csr, const mfg_layout* csc,
+                   int k, const void* vals_csr, const void* vals_csc, const void* W, int ldw,
+                   const void* H, int ldh, void* R, void* RH, void* RtW, double out_scale,
+                   double* sums, void* ws, size_t wsb, cudaStream_t stream) {
+  if (dtype == MFG_F64)
+    return do_sweep<double, double>(csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R, RH, RtW,
+                                     out_scale, sums, ws, wsb, stream);
+  if (compute_f64)
+    return do_sweep<float, double>(csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R, RH, RtW,
+                                    out_scale, sums, ws, wsb, stream);
+  return do_sweep<float, float>(csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R, RH, RtW,
+                                 out_scale, sums, ws, wsb, stream);
+}
+
+int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,
+                   int ldl, const double* scale, const void* Rt, int ldr, const void* A,
+                   const void* G, double out_mult, void* out, double* sums, void* ws, size_t wsb,
+                   cudaStream_t stream) {
+  if (dtype == MFG_F64)
+    return do_sddmm<double, double>(lay, k, L, ldl, scale, Rt, ldr, A, G, out_mult, out, sums, ws,
+                                     wsb, stream);
+  if (compute_f64)
+    return do_sddmm<float, double>(lay, k, L, ldl, scale, Rt, ldr, A, G, out_mult, out, sums, ws,
+                                    wsb, stream);
+  return do_sddmm<float, float>(lay, k, L, ldl, scale, Rt, ldr, A, G, out_mult, out, sums, ws,
+                                 wsb, stream);
+}
+
+}  // namespace mfg

@@ -1,0 +1,134 @@
+"""Nonconvex factorisation phase on the device (mirror of mfg/mfsolver.py).
+
+Lemma-1 factors, the MF objective (one fused Omega sweep), and exact
+block-coordinate descent whose per-row normal equations are assembled and
+solved inside libmfg_b200 (mfg_bcd_half_sweep) without ever materialising
+the (m, k, k) normal tensor of the reference.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .data import ObservationSet
+from .kernels import SIGMA_FLOOR, SvdTriplet, as_device
+from .operators import FactorPair
+
+_GUARD_SLACK = 1e-9          # mfg/mfsolver.py:15
+_GUARD_SLACK_F32 = 1e-6      # fp32 storage: rounding of the stored factors
+_PAIR_CHUNK = 1 << 25        # mfg/mfsolver.py:18 (API parity; unused on device)
+
+
+def guard_slack(dtype) -> float:
+    return _GUARD_SLACK if dtype == torch.float64 else _GUARD_SLACK_F32
+
+
+class MfPhaseError(RuntimeError):
+    """The BCD sweep increased the objective: indicates a kernel bug."""
+
+
+def factors_from_svd(x: SvdTriplet) -> FactorPair:
+    """W = U sqrt(s), H = V sqrt(s) (mfg/mfsolver.py:25-32)."""
+    root = torch.as_tensor(np.sqrt(x.sigma), device=x.u.device)
+    return FactorPair(x.u * root, x.v * root)
+
+
+def svd_from_factors(wf: FactorPair) -> SvdTriplet:
+    """Compact SVD of W H^T via QR of the factors and a k x k SVD (35-45)."""
+    if wf.k == 0:
+        return SvdTriplet.zero(wf.m, wf.n)
+    qw, rw = torch.linalg.qr(wf.w.double())
+    qh, rh = torch.linalg.qr(wf.h.double())
+    u_mid, s, vt_mid = torch.linalg.svd(rw @ rh.T)
+    sh = s.cpu().numpy()
+    if sh.size == 0 or sh[0] == 0.0:
+        return SvdTriplet.zero(wf.m, wf.n)
+    kept = np.flatnonzero(sh > SIGMA_FLOOR * sh[0])
+    idx = torch.as_tensor(kept, device=qw.device)
+    return SvdTriplet(qw @ u_mid.index_select(1, idx), sh[kept], qh @ vt_mid.T.index_select(1, idx))
+
+
+def sweep(obs: ObservationSet, wf: FactorPair, *, want_r=False, want_rh=False, want_rtw=False,
+          out_scale: float = 1.0, compute_f64: bool = True):
+    """One fused Omega sweep (mfg_sweep): R, R.H, R^T.W and fp64 sums.
+
+    Returns (R, RH, RtW, sums) with sums = [sum r^2, ||W||^2, ||H||^2] on the
+    host; unrequested outputs are None."""
+    dev = obs.dev
+    dt = obs.dtype
+    w = wf.w.to(dt).contiguous()
+    h = wf.h.to(dt).contiguous()
+    k = wf.k
+    R = torch.empty(obs.size, dtype=dt, device=dev.device) if want_r else None
+    RH = torch.empty((obs.m, k), dtype=dt, device=dev.device) if want_rh else None
+    RtW = torch.empty((obs.n, k), dtype=dt, device=dev.device) if want_rtw else None
+    sums = torch.empty(3, dtype=torch.float64, device=dev.device)
+    lib = _lib.lib()
+    wsb = lib.mfg_sweep_workspace(dev.csr.ref, dev.csc.ref, max(k, 1))
+    ws = dev.workspace(wsb)
+    _lib.check(lib.mfg_sweep(_lib.dtype_code(dt), 1 if compute_f64 else 0, dev.csr.ref, dev.csc.ref,
+                             max(k, 1), dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(),
+                             max(k, 1), h.data_ptr(), max(k, 1), _lib.ptr(R), _lib.ptr(RH),
+                             _lib.ptr(RtW), float(out_scale), sums.data_ptr(), ws.data_ptr(), wsb,
+                             _lib.stream_ptr()), "sweep")
+    return R, RH, RtW, sums.cpu().numpy()
+
+
+def mf_objective(obs: ObservationSet, wf: FactorPair, lam: float) -> float:
+    """f(W H^T) + (lam/2)(||W||^2 + ||H||^2) (mfg/mfsolver.py:48-50)."""
+    if wf.w.shape[0] != obs.m or wf.h.shape[0] != obs.n:
+        raise ValueError("factor dimensions do not match the data")
+    if wf.k == 0:
+        from .data import _dot
+        return _dot(obs.dev.vals64, obs.dev.vals64)
+    _, _, _, s = sweep(obs, wf)
+    return float(s[0]) + 0.5 * lam * (float(s[1]) + float(s[2]))
+
+
+def _half_sweep(obs: ObservationSet, transpose: bool, other: torch.Tensor, lam: float) -> torch.Tensor:
+    dev = obs.dev
+    lay = dev.csc if transpose else dev.csr
+    vals = dev.vals_csc if transpose else dev.vals
+    dt = obs.dtype
+    other = other.to(dt).contiguous()
+    k = int(other.shape[1])
+    out = torch.empty((lay.nrows, k), dtype=dt, device=dev.device)
+    lib = _lib.lib()
+    wsb = lib.mfg_bcd_workspace(lay.ref, k)
+    ws = dev.workspace(wsb)
+    _lib.check(lib.mfg_bcd_half_sweep(_lib.dtype_code(dt), lay.ref, k, vals.data_ptr(),
+                                      other.data_ptr(), k, float(lam), out.data_ptr(), k,
+                                      ws.data_ptr(), wsb, _lib.stream_ptr()), "bcd half sweep")
+    return out
+
+
+def bcd_epoch(obs: ObservationSet, wf: FactorPair, lam: float) -> FactorPair:
+    """All rows of W given H, then all rows of H given the new W (78-93)."""
+    if lam <= 0:
+        raise ValueError("lam must be positive")
+    if wf.w.shape[0] != obs.m or wf.h.shape[0] != obs.n:
+        raise ValueError("factor dimensions do not match the data")
+    if wf.k == 0:
+        return wf
+    w_new = _half_sweep(obs, False, wf.h, lam)
+    h_new = _half_sweep(obs, True, w_new, lam)
+    return FactorPair(w_new, h_new)
+
+
+def mf_phase(obs: ObservationSet, start: FactorPair, lam: float, epochs: int) -> FactorPair:
+    """``epochs`` BCD sweeps with the monotone-descent guard (96-112)."""
+    wf = start
+    if epochs <= 0:
+        return wf
+    wf = wf.to(obs.dtype)
+    slack = guard_slack(obs.dtype)
+    prev = mf_objective(obs, wf, lam)
+    for _ in range(epochs):
+        wf = bcd_epoch(obs, wf, lam)
+        cur = mf_objective(obs, wf, lam)
+        if cur > prev + slack * (1.0 + abs(prev)):
+            raise MfPhaseError(f"BCD sweep increased the objective: {prev!r} -> {cur!r}")
+        prev = cur
+    return wf
