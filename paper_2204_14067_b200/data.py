@@ -390,8 +390,13 @@ def residual_on_omega(obs: ObservationSet, wf: "FactorPair") -> SparseResidual:
             f"factor dims ({wf.w.shape[0]}, {wf.h.shape[0]}) do not match data "
             f"({obs.m}, {obs.n})"
         )
-    dt = obs.dtype
-    vals, sums = sddmm(obs, wf.w, wf.h, dtype=dt, compute_f64=True)
+    # Residuals (hence gradients) are stored in fp64 in both precision modes:
+    # they feed the lifting step, whose Eq. 5 test compares O(f) quantities
+    # with a 1e-12 relative slack. In fp32 mode the factors are fp32 and the
+    # products are formed exactly in fp64.
+    w = wf.w.to(obs.dtype).double()
+    h = wf.h.to(obs.dtype).double()
+    vals, sums = sddmm(obs, w, h, dtype=torch.float64)
     return SparseResidual(obs.m, obs.n, obs, vals, float(sums[0]))
 
 
