@@ -162,6 +162,13 @@ int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k,
 int mfg_dot(int dtype, int64_t count, const void* x, const void* y,
             double* out, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- diagnostics ------------------------------------------------------
+ * CUDA-event timing of the main sweep kernel on its launching stream, for
+ * the roofline figure of bench.py: enable with room for max_records
+ * launches (0 disables), then collect the summed milliseconds.            */
+int mfg_profile_enable(int max_records);
+int mfg_profile_collect(double* total_ms, int* count);
+
 #ifdef __cplusplus
 }
 #endif

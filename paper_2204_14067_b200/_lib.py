@@ -73,6 +73,8 @@ _SIGS = {
     "mfg_bcd_workspace": (_SZ, [_LP, _INT]),
     "mfg_bcd_half_sweep": (_INT, [_INT, _LP, _INT, _P, _P, _INT, _D, _P, _INT, _P, _SZ, _P]),
     "mfg_dot": (_INT, [_INT, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "mfg_profile_enable": (_INT, [_INT]),
+    "mfg_profile_collect": (_INT, [ctypes.POINTER(_D), ctypes.POINTER(_INT)]),
 }
 
 _lib = None

@@ -21,12 +21,33 @@
 //      step 2, and is flushed (coalesced k-vector store) at each row change.
 // This replaces pair_values (mfg/data.py:253-263, an einsum over gathered
 // rows) and scipy csr_matvecs (grad.csr @ block, mfg/operators.py:108,117).
+#include <vector>
+
 #include "common.cuh"
 #include "engine.cuh"
 
 namespace mfg {
 
 std::atomic<int64_t> g_launches{0};
+
+// Optional per-launch CUDA-event timing of the dominant (main sweep) kernel,
+// recorded on the launching stream. Enabled by mfg_profile_enable().
+struct KernelProfiler {
+  std::vector<cudaEvent_t> start, stop;
+  size_t used = 0;
+  bool on = false;
+};
+KernelProfiler g_prof;
+
+static void prof_begin(cudaStream_t s) {
+  if (g_prof.on && g_prof.used < g_prof.start.size()) cudaEventRecord(g_prof.start[g_prof.used], s);
+}
+static void prof_end(cudaStream_t s) {
+  if (g_prof.on && g_prof.used < g_prof.start.size()) {
+    cudaEventRecord(g_prof.stop[g_prof.used], s);
+    ++g_prof.used;
+  }
+}
 
 namespace {
 
@@ -506,8 +527,10 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
     const int n0 = csr->nnz ? P0.nchunks : 0;
     const int n1 = (acc1 && csc->nnz) ? P1.nchunks : 0;
     int st;
+    prof_begin(stream);
     if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
     else st = launch_main<TS, TC, false>(P0, P1, n0, 0, k, stream);
+    prof_end(stream);
     if (st != MFG_OK) return st;
     if (n0 == 0) {  // no entries: partials are zero
       MFG_CUDA_CHECK(cudaMemsetAsync(P0.part, 0, sizeof(double) * 3, stream));
@@ -609,3 +632,36 @@ int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, con
 }
 
 }  // namespace mfg
+
+extern "C" int mfg_profile_enable(int max_records) {
+  using mfg::g_prof;
+  for (auto e : g_prof.start) cudaEventDestroy(e);
+  for (auto e : g_prof.stop) cudaEventDestroy(e);
+  g_prof.start.clear();
+  g_prof.stop.clear();
+  g_prof.used = 0;
+  g_prof.on = max_records > 0;
+  for (int i = 0; i < max_records; ++i) {
+    cudaEvent_t a, b;
+    MFG_CUDA_CHECK(cudaEventCreate(&a));
+    MFG_CUDA_CHECK(cudaEventCreate(&b));
+    g_prof.start.push_back(a);
+    g_prof.stop.push_back(b);
+  }
+  return MFG_OK;
+}
+
+extern "C" int mfg_profile_collect(double* total_ms, int* count) {
+  using mfg::g_prof;
+  double t = 0.0;
+  for (size_t i = 0; i < g_prof.used; ++i) {
+    MFG_CUDA_CHECK(cudaEventSynchronize(g_prof.stop[i]));
+    float ms = 0.f;
+    MFG_CUDA_CHECK(cudaEventElapsedTime(&ms, g_prof.start[i], g_prof.stop[i]));
+    t += ms;
+  }
+  *total_ms = t;
+  *count = (int)g_prof.used;
+  g_prof.used = 0;
+  return MFG_OK;
+}

@@ -50,30 +50,54 @@ def svd_from_factors(wf: FactorPair) -> SvdTriplet:
     return SvdTriplet(qw @ u_mid.index_select(1, idx), sh[kept], qh @ vt_mid.T.index_select(1, idx))
 
 
+class SweepPlan:
+    """Pre-planned Omega sweep (mfg_sweep) with resident outputs and workspace.
+
+    ``run(w, h)`` enqueues one sweep on the current stream without any host
+    synchronisation; outputs land in ``R``, ``RH``, ``RtW`` and the fp64 device
+    vector ``sums`` = [sum r^2, ||W||^2, ||H||^2]. This is the unit of work of
+    the BASELINE metric."""
+
+    def __init__(self, obs: ObservationSet, k: int, *, want_r=True, want_rh=True, want_rtw=True,
+                 out_scale: float = 1.0, compute_f64: bool = False):
+        self.obs = obs
+        dev = obs.dev
+        dt = obs.dtype
+        self.k = int(k)
+        self.dt = dt
+        self.compute_f64 = 1 if compute_f64 else 0
+        self.out_scale = float(out_scale)
+        self.R = torch.empty(obs.size, dtype=dt, device=dev.device) if want_r else None
+        self.RH = torch.empty((obs.m, k), dtype=dt, device=dev.device) if want_rh else None
+        self.RtW = torch.empty((obs.n, k), dtype=dt, device=dev.device) if want_rtw else None
+        self.sums = torch.zeros(3, dtype=torch.float64, device=dev.device)
+        lib = _lib.lib()
+        self.wsb = lib.mfg_sweep_workspace(dev.csr.ref, dev.csc.ref, max(self.k, 1))
+        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=dev.device)
+
+    def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
+        dev = self.obs.dev
+        k = max(self.k, 1)
+        _lib.check(_lib.lib().mfg_sweep(
+            _lib.dtype_code(self.dt), self.compute_f64, dev.csr.ref, dev.csc.ref, k,
+            dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(), k, h.data_ptr(), k,
+            _lib.ptr(self.R), _lib.ptr(self.RH), _lib.ptr(self.RtW), self.out_scale,
+            self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, _lib.stream_ptr()), "sweep")
+
+
 def sweep(obs: ObservationSet, wf: FactorPair, *, want_r=False, want_rh=False, want_rtw=False,
           out_scale: float = 1.0, compute_f64: bool = True):
     """One fused Omega sweep (mfg_sweep): R, R.H, R^T.W and fp64 sums.
 
     Returns (R, RH, RtW, sums) with sums = [sum r^2, ||W||^2, ||H||^2] on the
     host; unrequested outputs are None."""
-    dev = obs.dev
     dt = obs.dtype
     w = wf.w.to(dt).contiguous()
     h = wf.h.to(dt).contiguous()
-    k = wf.k
-    R = torch.empty(obs.size, dtype=dt, device=dev.device) if want_r else None
-    RH = torch.empty((obs.m, k), dtype=dt, device=dev.device) if want_rh else None
-    RtW = torch.empty((obs.n, k), dtype=dt, device=dev.device) if want_rtw else None
-    sums = torch.empty(3, dtype=torch.float64, device=dev.device)
-    lib = _lib.lib()
-    wsb = lib.mfg_sweep_workspace(dev.csr.ref, dev.csc.ref, max(k, 1))
-    ws = dev.workspace(wsb)
-    _lib.check(lib.mfg_sweep(_lib.dtype_code(dt), 1 if compute_f64 else 0, dev.csr.ref, dev.csc.ref,
-                             max(k, 1), dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(),
-                             max(k, 1), h.data_ptr(), max(k, 1), _lib.ptr(R), _lib.ptr(RH),
-                             _lib.ptr(RtW), float(out_scale), sums.data_ptr(), ws.data_ptr(), wsb,
-                             _lib.stream_ptr()), "sweep")
-    return R, RH, RtW, sums.cpu().numpy()
+    plan = SweepPlan(obs, wf.k, want_r=want_r, want_rh=want_rh, want_rtw=want_rtw,
+                     out_scale=out_scale, compute_f64=compute_f64)
+    plan.run(w, h)
+    return plan.R, plan.RH, plan.RtW, plan.sums.cpu().numpy()
 
 
 def mf_objective(obs: ObservationSet, wf: FactorPair, lam: float) -> float:
