@@ -219,9 +219,10 @@ def main():
     k = spec.k0
     obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
     w_np, h_np = synth.sweep_factors(m, n, k, seed=1 + rank, dtype=np.float32)
-    w = torch.as_tensor(w_np, device=dev)
-    h = torch.as_tensor(h_np, device=dev)
     plan = SweepPlan(obs, k, compute_f64=False)
+    # resident factors in the grouped kernel's zero-padded layout
+    w = plan.pad(torch.as_tensor(w_np, device=dev))
+    h = plan.pad(torch.as_tensor(h_np, device=dev))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -293,12 +294,12 @@ def main():
     rh_host = torch.empty((m, k), dtype=torch.float32).pin_memory()
     rtw_host = torch.empty((n, k), dtype=torch.float32).pin_memory()
     sums_host = torch.empty(3, dtype=torch.float64).pin_memory()
-    w_dev = torch.empty_like(w)
-    h_dev = torch.empty_like(h)
+    w_dev = torch.zeros_like(w)
+    h_dev = torch.zeros_like(h)
 
     def e2e_step():
-        w_dev.copy_(w_host, non_blocking=True)
-        h_dev.copy_(h_host, non_blocking=True)
+        w_dev[:, :k].copy_(w_host, non_blocking=True)
+        h_dev[:, :k].copy_(h_host, non_blocking=True)
         plan.run(w_dev, h_dev)
         rh_host.copy_(plan.RH, non_blocking=True)
         rtw_host.copy_(plan.RtW, non_blocking=True)

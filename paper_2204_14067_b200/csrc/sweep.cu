@@ -88,8 +88,9 @@ struct Pass {
   double out_scale;
   int cb;               // batches per chunk
   int nchunks;
-  TC* carry_vec;        // [2*nchunks][k]
+  TC* carry_vec;        // [2*nchunks][cstride]
   int32_t* carry_row;   // [2*nchunks]
+  int cstride;          // carry vector stride (k, or the padded kp of the grouped kernel)
   double* part;         // [3][nchunks] per-warp partial sums (or null)
   int want_sq;          // accumulate sum r^2 into part[0]
 };
@@ -309,18 +310,492 @@ __device__ void run_chunk(const Pass<TS, TC>& P, int chunk, int k, int32_t* s_co
   }
 }
 
+// Out-of-line row flush (row ends are rare relative to entries): either a
+// direct coalesced store of the k-vector or a carry slot for a row that
+// crosses a chunk boundary.
+template <typename TS, typename TC>
+__device__ __noinline__ void flush_row(TS* out, int ldout, double out_scale, TC* carry_vec,
+                                       int64_t slot, int k, int frow, TC a0, TC a1) {
+  const int lane = threadIdx.x & 31;
+  const int d0 = lane, d1 = lane + 32;
+  if (slot >= 0) {
+    if (d0 < k) carry_vec[slot * k + d0] = a0;
+    if (d1 < k) carry_vec[slot * k + d1] = a1;
+  } else {
+    if (d0 < k) out[(int64_t)frow * ldout + d0] = (TS)(a0 * (TC)out_scale);
+    if (d1 < k) out[(int64_t)frow * ldout + d1] = (TS)(a1 * (TC)out_scale);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, T (&o)[4]);
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, float (&o)[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void ld4<double>(const double* p, double (&o)[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
+
+// Fast path (k <= 32*S): branch-free inner loops for batches that contain no
+// row start (the common case), next-batch index/value prefetch, vectorised
+// shared-memory broadcasts, and no per-slot validity tests (padding slots
+// gather row 0 and contribute r = 0).
+template <typename TS, typename TC, int S, bool ACC>
+__device__ __forceinline__ void run_chunk_fast(const Pass<TS, TC>& P, int chunk, int k,
+                                               int32_t* s_col, TC* s_r, int32_t* s_row) {
+  static_assert(S == 1 || S == 2, "S in {1,2}");
+  const int lane = lane_id();
+  const int64_t nnz = P.lay.nnz;
+  const int64_t E0 = (int64_t)chunk * P.cb * 32;
+  if (E0 >= nnz) return;
+  const int64_t E1 = min(E0 + (int64_t)P.cb * 32, nnz);
+  const int nb = (int)((E1 - E0 + 31) / 32);
+  const int32_t* __restrict__ idx = P.lay.idx;
+  const uint32_t* __restrict__ bm = P.lay.bmask;
+  const int32_t* __restrict__ nzrows = P.lay.nzrows;
+  const TS* __restrict__ vals = P.vals;
+  const TS* __restrict__ Gv = P.G;
+  const TS* __restrict__ other = P.other;
+  const TS* __restrict__ self = P.self;
+  const double* __restrict__ scale = P.scale;
+  const int ldo = P.ldo, lds = P.lds;
+  const int64_t b0 = E0 / 32;
+  const bool start_cross = (bm[b0] & 1u) == 0u;
+  const bool end_cross = (E1 < nnz) && ((bm[E1 / 32] & 1u) == 0u);
+  int rank = P.lay.brank[b0];
+  int row = nzrows[rank];
+  bool first_row = true;
+  int row_first = -1, row_last = -1;
+
+  TC w[S];
+  auto load_w = [&](int rw) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int d = lane + 32 * s;
+      TC v = TC(0);
+      if (d < k) {
+        v = (TC)self[(int64_t)rw * lds + d];
+        if (scale) v *= (TC)scale[d];
+      }
+      w[s] = v;
+    }
+  };
+  load_w(row);
+  TC acc[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) acc[s] = TC(0);
+  double sq = 0.0, s1 = 0.0, s2 = 0.0;
+
+  auto flush = [&](int frow, bool is_first, bool is_last) {
+    int64_t slot = -1;
+    if (is_first && start_cross) { slot = 2 * (int64_t)chunk; row_first = frow; }
+    else if (is_last && end_cross) { slot = 2 * (int64_t)chunk + 1; row_last = frow; }
+    flush_row<TS, TC>(P.out, P.ldout, P.out_scale, P.carry_vec, slot, k, frow, acc[0],
+                      S > 1 ? acc[S - 1] : TC(0));
+  };
+
+  int col_n = 0;
+  TC a_n = TC(0), g_n = TC(0);
+  uint32_t mask_n = 0u;
+  auto fetch = [&](int bi) {
+    const int64_t e = E0 + (int64_t)bi * 32 + lane;
+    const bool v = e < E1;
+    col_n = v ? idx[e] : 0;
+    a_n = (v && vals) ? (TC)vals[e] : TC(0);
+    g_n = (v && Gv) ? (TC)Gv[e] : TC(0);
+    mask_n = bm[b0 + bi];
+  };
+  fetch(0);
+
+  for (int bi = 0; bi < nb; ++bi) {
+    const int col = col_n;
+    const TC a = a_n, gval = g_n;
+    const uint32_t mask = mask_n & (bi == 0 ? ~1u : ~0u);
+    const int64_t Eb = E0 + (int64_t)bi * 32;
+    const int nvalid = (int)min((int64_t)32, E1 - Eb);
+    if (bi + 1 < nb) fetch(bi + 1);
+    __syncwarp();
+    s_col[lane] = col;
+    __syncwarp();
+
+    TS h[32][S];
+#pragma unroll
+    for (int t4 = 0; t4 < 32; t4 += 4) {
+      const int4 j4 = *reinterpret_cast<const int4*>(s_col + t4);
+      const int jj[4] = {j4.x, j4.y, j4.z, j4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const int d = lane + 32 * s;
+          h[t4 + u][s] = d < k ? other[(int64_t)jj[u] * ldo + d] : TS(0);
+        }
+      }
+    }
+    TC p[32];
+    const int row_b = row;
+    const bool fr_b = first_row;
+    if (mask == 0u) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        TC v = w[0] * (TC)h[t][0];
+        if (S > 1) v += w[S - 1] * (TC)h[t][S - 1];
+        p[t] = v;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if ((mask >> t) & 1u) {
+          ++rank;
+          row = nzrows[rank];
+          load_w(row);
+          s_row[t] = row;
+        }
+        TC v = w[0] * (TC)h[t][0];
+        if (S > 1) v += w[S - 1] * (TC)h[t][S - 1];
+        p[t] = v;
+      }
+    }
+    const TC dot = transpose_reduce(p);
+    const bool valid = lane < nvalid;
+    const TC r = valid ? dot - a : TC(0);
+    if (valid) {
+      if (P.R) P.R[Eb + lane] = (TS)(r * (TC)P.r_mult);
+      if (P.want_sq) sq += (double)r * (double)r;
+      if (Gv) {
+        s1 += (double)gval * ((double)r - 0.5 * (double)gval);
+        s2 += (double)gval * (double)dot;
+      }
+    }
+    if (ACC) {
+      __syncwarp();
+      s_r[lane] = r;
+      __syncwarp();
+      if (mask == 0u) {
+#pragma unroll
+        for (int t4 = 0; t4 < 32; t4 += 4) {
+          TC r4[4];
+          ld4<TC>(s_r + t4, r4);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] += r4[u] * (TC)h[t4 + u][s];
+        }
+      } else {
+        int rw = row_b;
+        bool fr = fr_b;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          if ((mask >> t) & 1u) {
+            flush(rw, fr, false);
+            fr = false;
+            rw = s_row[t];
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s] = TC(0);
+          }
+          const TC rt = s_r[t];
+#pragma unroll
+          for (int s = 0; s < S; ++s) acc[s] += rt * (TC)h[t][s];
+        }
+        first_row = fr;
+      }
+    } else if (mask != 0u) {
+      first_row = false;
+    }
+  }
+  if (ACC) {
+    flush(row, first_row, true);
+    if (lane == 0) {
+      P.carry_row[2 * chunk] = row_first;
+      P.carry_row[2 * chunk + 1] = row_last;
+    }
+  }
+  if (P.part) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      P.part[chunk] = sq;
+      P.part[P.nchunks + chunk] = s1;
+      P.part[2 * P.nchunks + chunk] = s2;
+    }
+  }
+}
+
 template <typename TS, typename TC, int S, bool ACC, bool MULTI>
 __global__ void __launch_bounds__(kThreads)
 k_sweep(Pass<TS, TC> P0, Pass<TS, TC> P1, int nw0, int nw_total, int k) {
-  __shared__ int32_t s_col[kWarpsPerBlock][32];
-  __shared__ TC s_r[kWarpsPerBlock][32];
+  __shared__ __align__(16) int32_t s_col[kWarpsPerBlock][32];
+  __shared__ __align__(16) TC s_r[kWarpsPerBlock][32];
+  __shared__ int32_t s_row[kWarpsPerBlock][32];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   const int wib = threadIdx.x >> 5;
   TC* s_acc = MULTI ? reinterpret_cast<TC*>(s_dyn) + (size_t)wib * k : nullptr;
   const int gw = blockIdx.x * kWarpsPerBlock + wib;
   if (gw >= nw_total) return;
-  if (gw < nw0) run_chunk<TS, TC, S, ACC, MULTI>(P0, gw, k, s_col[wib], s_r[wib], s_acc);
-  else run_chunk<TS, TC, S, ACC, MULTI>(P1, gw - nw0, k, s_col[wib], s_r[wib], s_acc);
+  if constexpr (!MULTI) {
+    if (gw < nw0) run_chunk_fast<TS, TC, S, ACC>(P0, gw, k, s_col[wib], s_r[wib], s_row[wib]);
+    else run_chunk_fast<TS, TC, S, ACC>(P1, gw - nw0, k, s_col[wib], s_r[wib], s_row[wib]);
+  } else {
+    if (gw < nw0) run_chunk<TS, TC, S, ACC, MULTI>(P0, gw, k, s_col[wib], s_r[wib], s_acc);
+    else run_chunk<TS, TC, S, ACC, MULTI>(P1, gw - nw0, k, s_col[wib], s_r[wib], s_acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// v3 "grouped" sweep: 8-lane groups act as independent mini-warps, each
+// owning a flat chunk of entries. Factor rows are zero-padded to kp = 8*V
+// elements, so lane q of a group holds dims [qV, qV+V) and ONE 16-byte vector
+// load per lane gathers a whole 128-byte row across the group (one L1
+// wavefront per entry, the minimum). Per 8-entry group-batch: 8 row gathers,
+// lane-partial dots, a 3-step butterfly (7 shuffles per 8 entries) that
+// leaves entry q's dot in lane q, then the SpMM accumulation from the same
+// registers. Row ends are rare and handled by an out-of-line flush.
+
+template <typename TS, typename TC, int V>
+__device__ __forceinline__ void ldrow(const TS* p, TS (&o)[V]) {
+  if constexpr (sizeof(TS) == 4) {
+#pragma unroll
+    for (int v4 = 0; v4 < V / 4; ++v4) {
+      const float4 x = reinterpret_cast<const float4*>(p)[v4];
+      o[4 * v4] = x.x; o[4 * v4 + 1] = x.y; o[4 * v4 + 2] = x.z; o[4 * v4 + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int v2 = 0; v2 < V / 2; ++v2) {
+      const double2 x = reinterpret_cast<const double2*>(p)[v2];
+      o[2 * v2] = x.x; o[2 * v2 + 1] = x.y;
+    }
+  }
+}
+
+// 8-lane transposed butterfly: lane q (of its group) ends with sum_lanes v[q].
+template <typename T>
+__device__ __forceinline__ T reduce8(T (&v)[8]) {
+  const int q = threadIdx.x & 7;
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool upper = (q & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const T send = upper ? v[i] : v[i + s];
+      const T keep = upper ? v[i + s] : v[i];
+      v[i] = keep + shfl_xor(send, s);
+    }
+  }
+  return v[0];
+}
+
+template <typename TC, int V>
+struct AccV {
+  TC a[V];
+};
+
+template <typename TS, typename TC, int V>
+__device__ __noinline__ void flush_group(TS* out, int ldout, double out_scale, TC* carry_vec,
+                                         int64_t slot, int k, int kp, int frow, AccV<TC, V> acc) {
+  const int q = threadIdx.x & 7;
+  if (slot >= 0) {
+    TC* c = carry_vec + slot * kp + q * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) c[v] = acc.a[v];
+  } else {
+    TS* o = out + (int64_t)frow * ldout;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int d = q * V + v;
+      if (d < k) o[d] = (TS)(acc.a[v] * (TC)out_scale);
+    }
+  }
+}
+
+template <typename TS, typename TC, int V>
+__device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int k, int kp,
+                                          int32_t* s_col, TC* s_r, int32_t* s_rows) {
+  const int q = threadIdx.x & 7;
+  const int64_t nnz = P.lay.nnz;
+  const int64_t CB = (int64_t)P.cb * 8;
+  const int64_t E0 = (int64_t)chunk * CB;
+  const bool active = chunk < P.nchunks && E0 < nnz;
+  const int64_t E1 = active ? min(E0 + CB, nnz) : E0;
+  const int32_t* __restrict__ idx = P.lay.idx;
+  const uint32_t* __restrict__ bm = P.lay.bmask;
+  const int32_t* __restrict__ nzrows = P.lay.nzrows;
+  const TS* __restrict__ vals = P.vals;
+  const TS* __restrict__ self = P.self;
+  const char* __restrict__ obase = reinterpret_cast<const char*>(P.other + q * V);
+  const uint32_t ostride = (uint32_t)kp * (uint32_t)sizeof(TS);
+  bool start_cross = false, end_cross = false;
+  int rank = 0, row = 0;
+  if (active) {
+    const uint32_t m0 = bm[E0 >> 5];
+    const int o0 = (int)(E0 & 31);
+    start_cross = ((m0 >> o0) & 1u) == 0u;
+    rank = P.lay.brank[E0 >> 5] + __popc(m0 & ~1u & ((2u << o0) - 1u));
+    row = nzrows[rank];
+    end_cross = (E1 < nnz) && (((bm[E1 >> 5] >> (E1 & 31)) & 1u) == 0u);
+  }
+  bool first_row = true;
+  int row_first = -1, row_last = -1;
+  TC w[V];
+  auto load_w = [&](int rw) {
+    TS t[V];
+    ldrow<TS, TC, V>(self + (int64_t)rw * kp + q * V, t);
+#pragma unroll
+    for (int v = 0; v < V; ++v) w[v] = (TC)t[v];
+  };
+  if (active) load_w(row);
+  else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) w[v] = TC(0);
+  }
+  AccV<TC, V> acc;
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc.a[v] = TC(0);
+  double sq = 0.0;
+
+  auto flush = [&](int frow, bool is_first, bool is_last) {
+    int64_t slot = -1;
+    if (is_first && start_cross) { slot = 2 * (int64_t)chunk; row_first = frow; }
+    else if (is_last && end_cross) { slot = 2 * (int64_t)chunk + 1; row_last = frow; }
+    flush_group<TS, TC, V>(P.out, P.ldout, P.out_scale, P.carry_vec, slot, k, kp, frow, acc);
+  };
+
+  int col_n = 0;
+  TC a_n = TC(0);
+  auto fetch = [&](int gb) {
+    const int64_t e = E0 + (int64_t)gb * 8 + q;
+    const bool v = e < E1;
+    col_n = v ? idx[e] : 0;
+    a_n = v ? (TC)vals[e] : TC(0);
+  };
+  fetch(0);
+  const int ngb = P.cb;  // warp-uniform trip count (inactive tails are masked)
+  for (int gb = 0; gb < ngb; ++gb) {
+    const int64_t Eb = E0 + (int64_t)gb * 8;
+    const int64_t rem = E1 - Eb;
+    const int nvalid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
+    const int col = col_n;
+    const TC a = a_n;
+    if (gb + 1 < ngb) fetch(gb + 1);
+    uint32_t bits = 0u;
+    if (nvalid > 0) bits = (bm[Eb >> 5] >> (Eb & 31)) & 0xFFu;
+    if (gb == 0) bits &= ~1u;
+    bits &= (1u << nvalid) - 1u;
+    __syncwarp();
+    s_col[q] = col;
+    __syncwarp();
+    int cols[8];
+    {
+      const int4 c0 = reinterpret_cast<const int4*>(s_col)[0];
+      const int4 c1 = reinterpret_cast<const int4*>(s_col)[1];
+      cols[0] = c0.x; cols[1] = c0.y; cols[2] = c0.z; cols[3] = c0.w;
+      cols[4] = c1.x; cols[5] = c1.y; cols[6] = c1.z; cols[7] = c1.w;
+    }
+    TS h[8][V];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
+    TC p[8];
+    const int row_b = row;
+    const bool fr_b = first_row;
+    if (bits == 0u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        TC v = TC(0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
+        p[i] = v;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if ((bits >> i) & 1u) {
+          ++rank;
+          row = nzrows[rank];
+          load_w(row);
+          s_rows[i] = row;
+        }
+        TC v = TC(0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
+        p[i] = v;
+      }
+    }
+    const TC dot = reduce8(p);
+    const bool valid = q < nvalid;
+    const TC r = valid ? dot - a : TC(0);
+    if (valid) {
+      if (P.R) P.R[Eb + q] = (TS)r;
+      if (P.want_sq) sq += (double)r * (double)r;
+    }
+    __syncwarp();
+    s_r[q] = r;
+    __syncwarp();
+    TC r8[8];
+    ld4<TC>(s_r, *reinterpret_cast<TC(*)[4]>(&r8[0]));
+    ld4<TC>(s_r + 4, *reinterpret_cast<TC(*)[4]>(&r8[4]));
+    if (bits == 0u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+    } else {
+      int rw = row_b;
+      bool fr = fr_b;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if ((bits >> i) & 1u) {
+          flush(rw, fr, false);
+          fr = false;
+          rw = s_rows[i];
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+      }
+      first_row = fr;
+    }
+  }
+  if (active) {
+    flush(row, first_row, true);
+    if (q == 0) {
+      P.carry_row[2 * chunk] = row_first;
+      P.carry_row[2 * chunk + 1] = row_last;
+    }
+  }
+  if (P.part) {
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (q == 0 && chunk < P.nchunks) {
+      P.part[chunk] = sq;
+      P.part[P.nchunks + chunk] = 0.0;
+      P.part[2 * P.nchunks + chunk] = 0.0;
+    }
+  }
+}
+
+template <typename TS, typename TC, int V>
+__global__ void __launch_bounds__(kThreads)
+k_sweep_g8(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp) {
+  __shared__ __align__(16) int32_t s_col[kThreads / 8][8];
+  __shared__ __align__(16) TC s_r[kThreads / 8][8];
+  __shared__ int32_t s_rows[kThreads / 8][8];
+  const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;  // global group id
+  const int wbase = gid & ~3;                                     // first group of this warp
+  if (wbase >= ntot) return;                                      // warp-uniform
+  const int gl = threadIdx.x >> 3;
+  if (wbase < n0p) run_group<TS, TC, V>(P0, gid, k, kp, s_col[gl], s_r[gl], s_rows[gl]);
+  else run_group<TS, TC, V>(P1, gid - n0p, k, kp, s_col[gl], s_r[gl], s_rows[gl]);
 }
 
 // Epilogue: carries, empty rows, deterministic reductions.
@@ -341,25 +816,35 @@ template <typename TS, typename TC>
 __device__ void carry_fixup(const Pass<TS, TC>& P, int k, int warp_global, int nwarps_grid) {
   const int lane = lane_id();
   const int nslots = 2 * P.nchunks;
+  const int cs = P.cstride;
+  // Heads are the used odd slots (a row's last chunk-crossing); the run of
+  // slots carrying the same row follows in slot order (unused slots = -1).
   for (int q = 2 * warp_global + 1; q < nslots; q += 2 * nwarps_grid) {
     const int row = P.carry_row[q];
     if (row < 0) continue;
+    // find the run end with a warp-wide scan of the next 32 slots at a time
+    int end = q + 1;
+    while (end < nslots) {
+      const int sidx = end + lane;
+      const int r2 = sidx < nslots ? P.carry_row[sidx] : -2;
+      const bool stop = (sidx >= nslots) || (r2 >= 0 && r2 != row);
+      const unsigned b = __ballot_sync(0xffffffffu, stop);
+      if (b) { end += __ffs(b) - 1; break; }
+      end += 32;
+    }
+    if (end > nslots) end = nslots;
     for (int d0 = 0; d0 < k; d0 += 32) {
       const int d = d0 + lane;
       TC v = TC(0);
-      if (d < k) v = P.carry_vec[(int64_t)q * k + d];
-      for (int nx = q + 1; nx < nslots; ++nx) {
-        const int r2 = P.carry_row[nx];
-        if (r2 < 0) continue;
-        if (r2 != row) break;
-        if (d < k) v += P.carry_vec[(int64_t)nx * k + d];
+      if (d < k) {
+#pragma unroll 4
+        for (int sl = q; sl < end; ++sl) {
+          if (P.carry_row[sl] == row) v += P.carry_vec[(int64_t)sl * cs + d];
+        }
+        P.out[(int64_t)row * P.ldout + d] = (TS)(v * (TC)P.out_scale);
       }
-      if (d < k) P.out[(int64_t)row * P.ldout + d] = (TS)(v * (TC)P.out_scale);
     }
   }
-  // rows whose only contribution came through a start-crossing slot cannot
-  // occur: a start crossing implies the previous chunk's end crossing (an odd
-  // head slot) or a single-row previous chunk whose run began earlier.
   for (int i = warp_global; i < P.lay.n_empty; i += nwarps_grid) {
     const int row2 = P.lay.empty_rows[i];
     for (int d = lane; d < k; d += 32) P.out[(int64_t)row2 * P.ldout + d] = TS(0);
@@ -410,12 +895,15 @@ k_epilogue(Pass<TS, TC> P0, int has0, Pass<TS, TC> P1, int has1, int k, SumJob J
     last = (done == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x < 5) {
+  if (last) {
     __threadfence();
-    double s = 0.0;
     const volatile double* bp = J.block_part;
-    for (unsigned int b = 0; b < gridDim.x; ++b) s += bp[b * 5 + threadIdx.x];
-    J.sums[threadIdx.x] = s;
+    for (int c = 0; c < 5; ++c) {
+      double t = 0.0;
+      for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += bp[b * 5 + c];
+      const double tot = block_sum<256>(t, sm);
+      if (threadIdx.x == 0) J.sums[c] = tot;
+    }
     if (threadIdx.x == 0) *J.counter = 0u;
   }
 }
@@ -435,13 +923,36 @@ int chunks_of(int64_t nnz, int cb) {
   return (int)((nnz + (int64_t)cb * 32 - 1) / ((int64_t)cb * 32));
 }
 
+// Grouped (v3) kernel: padded factor width for k, or 0 if not eligible.
+int grouped_kp(int k, int elem_bytes) {
+  if (elem_bytes == 4) return k <= 32 ? 32 : (k <= 64 ? 64 : 0);
+  return k <= 16 ? 16 : (k <= 32 ? 32 : 0);
+}
+
+int pick_cb_g(int64_t nnz) {
+  const int64_t target = (int64_t)kNumSMs * 96;  // ~24 warps x 4 groups per SM
+  int64_t cb = (nnz + 8 * target - 1) / (8 * target);
+  if (cb < 4) cb = 4;
+  if (cb > 256) cb = 256;
+  return (int)cb;
+}
+
+int chunks_of_g(int64_t nnz, int cb) {
+  return (int)((nnz + (int64_t)cb * 8 - 1) / ((int64_t)cb * 8));
+}
+
 template <typename C>
 void carve_pass(C& c, const mfg_layout* lay, int k, bool acc, bool part) {
   if (!lay) return;
+  // room for either schedule: warp chunks (stride k) or group chunks (stride kp)
   const int cb = pick_cb(lay->nnz);
-  const int nch = chunks_of(lay->nnz, cb) > 0 ? chunks_of(lay->nnz, cb) : 1;
+  int64_t nch = chunks_of(lay->nnz, cb) > 0 ? chunks_of(lay->nnz, cb) : 1;
+  const int kp = grouped_kp(k, 4) ? grouped_kp(k, 4) : k;
+  const int64_t nchg = chunks_of_g(lay->nnz, pick_cb_g(lay->nnz)) + 4;
+  const size_t carry = (size_t)2 * (nch * k > nchg * kp ? nch * k : nchg * kp);
+  if (nchg > nch) nch = nchg;
   if (acc) {
-    c.template take<double>((size_t)2 * nch * k);  // carry vecs (sized for fp64)
+    c.template take<double>(carry);  // carry vecs (sized for fp64)
     c.template take<int32_t>((size_t)2 * nch);
   }
   if (part) c.template take<double>((size_t)3 * nch);
@@ -455,20 +966,52 @@ void carve_epi(C& c) {
 }
 
 template <typename TS, typename TC>
-bool setup_pass(Pass<TS, TC>& P, Carver& c, const mfg_layout* lay, int k, bool acc, bool part) {
+bool setup_pass(Pass<TS, TC>& P, Carver& c, const mfg_layout* lay, int k, bool acc, bool part,
+                int kp_grouped = 0) {
   P.lay = *lay;
-  P.cb = pick_cb(lay->nnz);
-  P.nchunks = chunks_of(lay->nnz, P.cb);
+  if (kp_grouped) {
+    P.cb = pick_cb_g(lay->nnz);
+    P.nchunks = chunks_of_g(lay->nnz, P.cb);
+    P.cstride = kp_grouped;
+  } else {
+    P.cb = pick_cb(lay->nnz);
+    P.nchunks = chunks_of(lay->nnz, P.cb);
+    P.cstride = k;
+  }
   const int nch = P.nchunks > 0 ? P.nchunks : 1;
   P.carry_vec = nullptr;
   P.carry_row = nullptr;
   P.part = nullptr;
   if (acc) {
-    P.carry_vec = reinterpret_cast<TC*>(c.take<double>((size_t)2 * nch * k));
+    P.carry_vec = reinterpret_cast<TC*>(c.take<double>((size_t)2 * nch * P.cstride));
     P.carry_row = c.take<int32_t>((size_t)2 * nch);
   }
   if (part) P.part = c.take<double>((size_t)3 * nch);
   return c.ok;
+}
+
+template <typename TS, typename TC>
+int launch_grouped(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k, int kp,
+                   cudaStream_t stream) {
+  const int n0p = (P0.nchunks + 3) & ~3;
+  const int n1p = (P1.nchunks + 3) & ~3;
+  const int ntot = n0p + n1p;
+  if (ntot == 0) return MFG_OK;
+  const int groups_per_block = kThreads / 8;
+  const int grid = (ntot + groups_per_block - 1) / groups_per_block;
+  const int V = kp / 8;
+  constexpr bool f32 = sizeof(TS) == 4, mixed = sizeof(TS) != sizeof(TC);
+  if constexpr (f32 && !mixed) {
+    if (V == 4) k_sweep_g8<TS, TC, 4><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+    else k_sweep_g8<TS, TC, 8><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+  } else if constexpr (f32) {
+    k_sweep_g8<TS, TC, 4><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+  } else {
+    if (V == 2) k_sweep_g8<TS, TC, 2><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+    else k_sweep_g8<TS, TC, 4><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+  }
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
 }
 
 template <typename TS, typename TC, bool ACC>
@@ -502,8 +1045,12 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
   Carver c(ws, wsb);
   Pass<TS, TC> P0{}, P1{};
   const bool acc0 = RH != nullptr, acc1 = RtW != nullptr;
-  if (!setup_pass(P0, c, csr, k, acc0, true)) goto small;
-  if (!setup_pass(P1, c, csc, k, acc1, false)) goto small;
+  // grouped v3 kernel: zero-padded factors of width kp, all outputs wanted
+  int kpg = grouped_kp(k, (int)sizeof(TS));
+  if (sizeof(TS) != sizeof(TC) && kpg > 32) kpg = 0;  // fp64 compute on fp32: V = 4 only
+  const bool grouped = kpg && ldw == kpg && ldh == kpg && acc0 && acc1 && csr->nnz > 0;
+  if (!setup_pass(P0, c, csr, k, acc0, true, grouped ? kpg : 0)) goto small;
+  if (!setup_pass(P1, c, csc, k, acc1, false, grouped ? kpg : 0)) goto small;
   {
     P0.vals = (const TS*)vals_csr; P0.G = nullptr; P0.self = (const TS*)W; P0.lds = ldw;
     P0.scale = nullptr; P0.other = (const TS*)H; P0.ldo = ldh; P0.R = (TS*)R; P0.r_mult = 1.0;
@@ -517,18 +1064,20 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
     double* tmp = c.take<double>(5);
     if (!c.ok) goto small;
     J.part = P0.part; J.np = P0.nchunks;
-    J.W = W; J.wcount = (ldw == k) ? (int64_t)csr->nrows * k : 0;
-    J.H = H; J.hcount = (ldh == k) ? (int64_t)csc->nrows * k : 0;
+    // norms over the ld-strided buffers: padding columns must be zero
+    J.W = W; J.wcount = (int64_t)csr->nrows * ldw;
+    J.H = H; J.hcount = (int64_t)csc->nrows * ldh;
     J.is_f64 = sizeof(TS) == 8;
     J.sums = tmp;
-    if (ldw != k || ldh != k) { set_error("sweep requires ldw == ldh == k"); return MFG_ERR_ARG; }
+    if (ldw < k || ldh < k) { set_error("sweep requires ldw, ldh >= k"); return MFG_ERR_ARG; }
     // counter must start at zero: the epilogue's last block re-zeroes it.
     MFG_CUDA_CHECK(cudaMemsetAsync(J.counter, 0, sizeof(unsigned int), stream));
     const int n0 = csr->nnz ? P0.nchunks : 0;
     const int n1 = (acc1 && csc->nnz) ? P1.nchunks : 0;
     int st;
     prof_begin(stream);
-    if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
+    if (grouped) st = launch_grouped<TS, TC>(P0, P1, k, kpg, stream);
+    else if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
     else st = launch_main<TS, TC, false>(P0, P1, n0, 0, k, stream);
     prof_end(stream);
     if (st != MFG_OK) return st;

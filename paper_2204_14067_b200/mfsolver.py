@@ -50,6 +50,15 @@ def svd_from_factors(wf: FactorPair) -> SvdTriplet:
     return SvdTriplet(qw @ u_mid.index_select(1, idx), sh[kept], qh @ vt_mid.T.index_select(1, idx))
 
 
+def grouped_width(k: int, dtype, compute_f64: bool = False) -> int:
+    """Padded factor width of the grouped sweep kernel for k (0 = not used)."""
+    if dtype == torch.float32:
+        if compute_f64:
+            return 32 if k <= 32 else 0
+        return 32 if k <= 32 else (64 if k <= 64 else 0)
+    return 16 if k <= 16 else (32 if k <= 32 else 0)
+
+
 class SweepPlan:
     """Pre-planned Omega sweep (mfg_sweep) with resident outputs and workspace.
 
@@ -74,13 +83,25 @@ class SweepPlan:
         lib = _lib.lib()
         self.wsb = lib.mfg_sweep_workspace(dev.csr.ref, dev.csc.ref, max(self.k, 1))
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=dev.device)
+        self.kp = grouped_width(self.k, dt, compute_f64)
+
+    def pad(self, f: torch.Tensor) -> torch.Tensor:
+        """Zero-padded (rows x kp) copy of a factor: the layout of the grouped
+        sweep kernel (one 16-byte vector per lane gathers a whole row)."""
+        if not self.kp:
+            return f.to(self.dt).contiguous()
+        out = torch.zeros((f.shape[0], self.kp), dtype=self.dt, device=self.obs.dev.device)
+        out[:, : f.shape[1]] = f
+        return out
 
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
+        """w, h: (rows x ld) with ld = k, or the zero-padded width ``kp``."""
         dev = self.obs.dev
         k = max(self.k, 1)
         _lib.check(_lib.lib().mfg_sweep(
             _lib.dtype_code(self.dt), self.compute_f64, dev.csr.ref, dev.csc.ref, k,
-            dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(), k, h.data_ptr(), k,
+            dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(), int(w.stride(0)),
+            h.data_ptr(), int(h.stride(0)),
             _lib.ptr(self.R), _lib.ptr(self.RH), _lib.ptr(self.RtW), self.out_scale,
             self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, _lib.stream_ptr()), "sweep")
 

@@ -202,3 +202,34 @@ def test_sweep_deterministic_and_identities():
     ra = float((R.double() * (R.double() + obs.dev.vals.double())).sum())
     assert lhs == pytest.approx(rhs, rel=1e-4)
     assert lhs == pytest.approx(ra, rel=1e-4)
+
+
+@pytest.mark.parametrize("k", [3, 8, 16, 20, 30, 32, 40, 64])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_grouped_sweep_vs_oracle(k, dtype):
+    """The grouped (zero-padded, 8-lane group) sweep kernel."""
+    from paper_2204_14067_b200.mfsolver import SweepPlan
+    m, n, r, c, v = synth.generate("c3", scale=0.03, seed=100 + k)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    om = orc.from_coo(m, n, r, c, v)
+    w, h = synth.sweep_factors(m, n, k, seed=k)
+    obs = D.ObservationSet.from_coo(m, n, r, c, v, dtype=dtype)
+    plan = SweepPlan(obs, k)
+    wt = torch.as_tensor(w).to(dtype).cuda()
+    ht = torch.as_tensor(h).to(dtype).cuda()
+    plan.run(plan.pad(wt), plan.pad(ht))
+    rr, rh, rtw, sq, w2, h2 = orc.sweep(om, _np(wt), _np(ht))
+    tol = 1e-11 if dtype == torch.float64 else 2e-5
+    sc = lambda a: max(1.0, np.abs(a).max())  # noqa: E731
+    amp = 1 if dtype == torch.float64 else 10
+    assert np.max(np.abs(_np(plan.R) - rr)) <= tol * sc(rr)
+    assert np.max(np.abs(_np(plan.RH) - rh)) <= tol * amp * sc(rh)
+    assert np.max(np.abs(_np(plan.RtW) - rtw)) <= tol * amp * sc(rtw)
+    sums = plan.sums.cpu().numpy()
+    assert sums[0] == pytest.approx(sq, rel=tol * 10)
+    assert sums[1] == pytest.approx(w2, rel=1e-12)
+    assert sums[2] == pytest.approx(h2, rel=1e-12)
+    # run-to-run bitwise determinism
+    R0, RH0 = plan.R.clone(), plan.RH.clone()
+    plan.run(plan.pad(wt), plan.pad(ht))
+    assert torch.equal(R0, plan.R) and torch.equal(RH0, plan.RH)
