@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="bounded CPU-baseline sample (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
+                    help="L2 flush between steps: write (zero 512 MiB), read (sum 512 MiB) or none")
     return ap.parse_args()
 
 
@@ -223,8 +225,15 @@ def main():
     # resident factors in the grouped kernel's zero-padded layout
     w = plan.pad(torch.as_tensor(w_np, device=dev))
     h = plan.pad(torch.as_tensor(h_np, device=dev))
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.zeros(512 << 20, dtype=torch.uint8, device=dev)
+    flush_i = flush.view(torch.int32)
     stream = torch.cuda.current_stream()
+
+    def do_flush():
+        if args.flush == "write":
+            flush.zero_()
+        elif args.flush == "read":
+            torch.sum(flush_i)
 
     # launches per sweep (our kernels), from one eager call
     c0 = lib.mfg_launch_count()
@@ -256,7 +265,7 @@ def main():
         torch.cuda.synchronize()
         t0 = time.time()
         for a, b in evs:
-            flush.zero_()
+            do_flush()
             a.record(stream)
             fn()
             b.record(stream)
@@ -268,7 +277,7 @@ def main():
         return sum(a.elapsed_time(b) for a, b in evs)
 
     for _ in range(args.warmup):
-        flush.zero_()
+        do_flush()
         g.replay()
     ms_total = timed(g.replay, args.steps)
     # max over ranks
@@ -310,7 +319,7 @@ def main():
         e2e_step()
     torch.cuda.synchronize()
     for _ in range(args.steps):
-        flush.zero_()
+        do_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         e2e_step()
@@ -372,7 +381,9 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 reductions)",
         "data": "synthetic",
         "config": {"workload": args.workload, "m": m, "n": n, "nnz": int(obs.size), "k": k,
-                   "values": "fp32", "l2": "flushed before every step (512 MiB write)",
+                   "values": "fp32", "l2": {"write": "flushed before every step (512 MiB write)",
+                          "read": "flushed before every step (512 MiB read)",
+                          "none": "not flushed (L2-warm)"}[args.flush],
                    "timing": "per-step CUDA events, CUDA-graph replay of the sweep",
                    "parallelism": f"{world} independent partitions (one per GPU)"},
         "e2e": {"value": e2e_value, "unit": UNIT,

@@ -16,6 +16,9 @@
  *    MFG_F32 (float) or MFG_F64 (double). Reductions are always fp64.
  *  - Dense matrices are row-major with a leading dimension (elements).
  *  - Omega indices are int32 (|Omega| < 2^31; checked at build time).
+ *  - Entry-stream arrays (layout idx / row_of and the value arrays passed to
+ *    mfg_sweep) must be readable for 64 entries past nnz (zero padding):
+ *    the grouped sweep kernel prefetches without bounds guards.
  */
 #ifndef MFG_B200_H
 #define MFG_B200_H
@@ -112,7 +115,12 @@ int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src,
  * recomputes r from its own value copy instead of gathering R).
  * Any of R/RH/RtW may be NULL to skip that output. out_scale multiplies
  * RH and RtW (e.g. 2 for gradients). vals_csc is A in CSC order.
- * compute_f64 != 0 forces fp64 arithmetic on f32 storage.                 */
+ * compute_f64 != 0 forces fp64 arithmetic on f32 storage.
+ * ldw/ldh >= k; padding columns must be zero. With ldw == ldh == the
+ * grouped width (32/64 for f32, 16/32 for f64) the single-launch grouped
+ * kernel runs (row pieces finished in-kernel, last-block fp64 reductions).
+ * The workspace must be zero-filled before its first use and not shared
+ * with concurrent calls; the sweep leaves its counters zeroed.           */
 size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);
 int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr,
               const mfg_layout* csc, int k, const void* vals_csr,
@@ -168,6 +176,9 @@ int mfg_dot(int dtype, int64_t count, const void* x, const void* y,
  * launches (0 disables), then collect the summed milliseconds.            */
 int mfg_profile_enable(int max_records);
 int mfg_profile_collect(double* total_ms, int* count);
+/* per-worker clock64 stamps of the grouped sweep (start, init, loop, end),
+ * [workers][4] int64 on the device; NULL disables.                        */
+int mfg_set_probe(void* dev_buffer);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmfg_b200.so")
+LIB_PATH = os.environ.get("MFG_LIB_PATH") or os.path.join(HERE, "libmfg_b200.so")
 
 MFG_OK, MFG_ERR_ARG, MFG_ERR_DATASET, MFG_ERR_CAPACITY, MFG_ERR_CUDA, MFG_ERR_NUMERICAL = range(6)
 MFG_F32, MFG_F64 = 0, 1
@@ -75,6 +75,7 @@ _SIGS = {
     "mfg_dot": (_INT, [_INT, _I64, _P, _P, _P, _P, _SZ, _P]),
     "mfg_profile_enable": (_INT, [_INT]),
     "mfg_profile_collect": (_INT, [ctypes.POINTER(_D), ctypes.POINTER(_INT)]),
+    "mfg_set_probe": (_INT, [_P]),
 }
 
 _lib = None

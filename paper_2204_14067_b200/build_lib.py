@@ -16,7 +16,7 @@ OUT = os.path.join(HERE, "libmfg_b200.so")
 OBJDIR = os.path.join(HERE, "build")
 SOURCES = ["abi.cu", "omega_build.cu", "sweep.cu", "spmm.cu", "bcd.cu", "dense.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = [*os.environ.get("MFG_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
 
 

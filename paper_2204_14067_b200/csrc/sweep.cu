@@ -21,7 +21,12 @@
 //      step 2, and is flushed (coalesced k-vector store) at each row change.
 // This replaces pair_values (mfg/data.py:253-263, an einsum over gathered
 // rows) and scipy csr_matvecs (grad.csr @ block, mfg/operators.py:108,117).
+#include <cstdlib>
 #include <vector>
+
+#ifndef MFG_G8_MINB
+#define MFG_G8_MINB 2
+#endif
 
 #include "common.cuh"
 #include "engine.cuh"
@@ -38,6 +43,7 @@ struct KernelProfiler {
   bool on = false;
 };
 KernelProfiler g_prof;
+long long* g_probe = nullptr;  // device buffer for per-worker clock stamps (diagnostics)
 
 static void prof_begin(cudaStream_t s) {
   if (g_prof.on && g_prof.used < g_prof.start.size()) cudaEventRecord(g_prof.start[g_prof.used], s);
@@ -91,6 +97,8 @@ struct Pass {
   TC* carry_vec;        // [2*nchunks][cstride]
   int32_t* carry_row;   // [2*nchunks]
   int cstride;          // carry vector stride (k, or the padded kp of the grouped kernel)
+  int32_t* row_cnt;     // [nrows] arrival counters (fused finisher; zero at rest)
+  long long* probe;     // optional [nchunks][4] clock64 stamps (diagnostics)
   double* part;         // [3][nchunks] per-warp partial sums (or null)
   int want_sq;          // accumulate sum r^2 into part[0]
 };
@@ -577,6 +585,15 @@ __device__ __forceinline__ void ldrow(const TS* p, TS (&o)[V]) {
   }
 }
 
+// cp.async (LDGSTS) 16-byte copy global -> shared, cached in L1 (.ca).
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // 8-lane transposed butterfly: lane q (of its group) ends with sum_lanes v[q].
 template <typename T>
 __device__ __forceinline__ T reduce8(T (&v)[8]) {
@@ -617,38 +634,101 @@ __device__ __noinline__ void flush_group(TS* out, int ldout, double out_scale, T
   }
 }
 
+// A worker deposited its piece of a row that crosses chunk boundaries into
+// carry slot `slot`. The worker that deposits the row's last piece sums all
+// pieces in slot order (first chunk a: slot 2a+1; chunks a+1..b: slot 2c)
+// and writes the output row, so no epilogue pass is needed and the result
+// is independent of arrival order.
+template <typename TS, typename TC, int V>
+__device__ __noinline__ void finish_row(TS* out, int ldout, double out_scale, TC* carry_vec,
+                                        int32_t* row_cnt, const int32_t* ptr, int64_t CB,
+                                        int k, int kp, int frow) {
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 7;
+  const unsigned gmask = 0xFFu << (lane & 24);
+  // Ordering: the group's carry stores -> warp barrier -> release fence
+  // (MEMBAR.GPU: stores acknowledged by L2, no L1 invalidation) -> counter
+  // increment. The finisher reads the pieces through L2 (ld.cg) after its
+  // own increment returned, so it observes every earlier piece. A
+  // __threadfence() here would also emit CCTL.IVALL and flush the SM's L1
+  // (the gathered factor rows) at every row crossing.
+  int old = 0;
+  if (q == 0) old = atomicAdd(&row_cnt[frow], 1);
+  old = __shfl_sync(gmask, old, lane & 24);
+  const int64_t a = (int64_t)ptr[frow] / CB;
+  const int64_t b = (int64_t)(ptr[frow + 1] - 1) / CB;
+  if (old != (int)(b - a)) return;
+  TC acc[V];
+  {
+    const TC* c = carry_vec + (2 * a + 1) * kp + q * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = __ldcg(c + v);
+  }
+  // pieces of chunks a+1..b: issue 8 pieces' loads at a time (independent,
+  // in flight together), then add them in slot order (deterministic)
+  int64_t ch = a + 1;
+  for (; ch + 8 <= b + 1; ch += 8) {
+    TC t[8][V];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const TC* c = carry_vec + (2 * (ch + u)) * kp + q * V;
+#pragma unroll
+      for (int v = 0; v < V; ++v) t[u][v] = __ldcg(c + v);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] += t[u][v];
+  }
+  for (; ch <= b; ++ch) {
+    const TC* c = carry_vec + (2 * ch) * kp + q * V;
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] += __ldcg(c + v);
+  }
+  TS* o = out + (int64_t)frow * ldout;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int d = q * V + v;
+    if (d < k) o[d] = (TS)(acc[v] * (TC)out_scale);
+  }
+  if (q == 0) row_cnt[frow] = 0;
+}
+
+// Lean grouped worker. Preconditions (checked by the launcher): chunk size
+// CB is a multiple of 32 entries; idx / row_of / vals are readable up to
+// nnz + 64 entries (the Omega arrays are allocated with that padding), so
+// the prefetch loads need no bounds guards. Entry offsets are 32-bit.
 template <typename TS, typename TC, int V>
 __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int k, int kp,
-                                          int32_t* s_col, TC* s_r, int32_t* s_rows) {
+                                          int32_t* s_ring, TS* s_vring, TC* s_r) {
   const int q = threadIdx.x & 7;
-  const int64_t nnz = P.lay.nnz;
-  const int64_t CB = (int64_t)P.cb * 8;
-  const int64_t E0 = (int64_t)chunk * CB;
+  const int nnz = (int)P.lay.nnz;
+  const int CB = P.cb * 8;
+  const int E0 = chunk * CB;
   const bool active = chunk < P.nchunks && E0 < nnz;
-  const int64_t E1 = active ? min(E0 + CB, nnz) : E0;
-  const int32_t* __restrict__ idx = P.lay.idx;
-  const uint32_t* __restrict__ bm = P.lay.bmask;
-  const int32_t* __restrict__ nzrows = P.lay.nzrows;
-  const TS* __restrict__ vals = P.vals;
-  const TS* __restrict__ self = P.self;
+  const int E1 = active ? min(E0 + CB, nnz) : E0;
+  const int32_t* __restrict__ pidx = P.lay.idx + E0 + q;
+  const int32_t* __restrict__ prow = P.lay.row_of + E0 + q;
+  const TS* __restrict__ pval = P.vals + E0 + q;
+  const uint32_t* __restrict__ pbm = P.lay.bmask + (E0 >> 5);
+  const TS* __restrict__ self = P.self + q * V;
   const char* __restrict__ obase = reinterpret_cast<const char*>(P.other + q * V);
   const uint32_t ostride = (uint32_t)kp * (uint32_t)sizeof(TS);
+  const int nvalid_all = E1 - E0;  // entries of this worker
   bool start_cross = false, end_cross = false;
-  int rank = 0, row = 0;
+  int row = 0;
+  long long t_start = clock64();
   if (active) {
-    const uint32_t m0 = bm[E0 >> 5];
-    const int o0 = (int)(E0 & 31);
-    start_cross = ((m0 >> o0) & 1u) == 0u;
-    rank = P.lay.brank[E0 >> 5] + __popc(m0 & ~1u & ((2u << o0) - 1u));
-    row = nzrows[rank];
-    end_cross = (E1 < nnz) && (((bm[E1 >> 5] >> (E1 & 31)) & 1u) == 0u);
+    start_cross = (pbm[0] & 1u) == 0u;
+    row = P.lay.row_of[E0];
+    end_cross = (E1 < nnz) && (((P.lay.bmask[E1 >> 5] >> (E1 & 31)) & 1u) == 0u);
   }
   bool first_row = true;
   int row_first = -1, row_last = -1;
   TC w[V];
   auto load_w = [&](int rw) {
     TS t[V];
-    ldrow<TS, TC, V>(self + (int64_t)rw * kp + q * V, t);
+    ldrow<TS, TC, V>(self + (int64_t)rw * kp, t);
 #pragma unroll
     for (int v = 0; v < V; ++v) w[v] = (TC)t[v];
   };
@@ -657,11 +737,15 @@ __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int 
 #pragma unroll
     for (int v = 0; v < V; ++v) w[v] = TC(0);
   }
+  long long t_init = 0, t_loop = 0;
+  if (P.probe) {
+    asm volatile("" ::"f"((float)w[0]));
+    t_init = clock64();
+  }
   AccV<TC, V> acc;
 #pragma unroll
   for (int v = 0; v < V; ++v) acc.a[v] = TC(0);
   double sq = 0.0;
-
   auto flush = [&](int frow, bool is_first, bool is_last) {
     int64_t slot = -1;
     if (is_first && start_cross) { slot = 2 * (int64_t)chunk; row_first = frow; }
@@ -669,136 +753,174 @@ __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int 
     flush_group<TS, TC, V>(P.out, P.ldout, P.out_scale, P.carry_vec, slot, k, kp, frow, acc);
   };
 
-  int col_n = 0;
-  TC a_n = TC(0);
-  auto fetch = [&](int gb) {
-    const int64_t e = E0 + (int64_t)gb * 8 + q;
-    const bool v = e < E1;
-    col_n = v ? idx[e] : 0;
-    a_n = v ? (TC)vals[e] : TC(0);
-  };
-  fetch(0);
-  const int ngb = P.cb;  // warp-uniform trip count (inactive tails are masked)
-  for (int gb = 0; gb < ngb; ++gb) {
-    const int64_t Eb = E0 + (int64_t)gb * 8;
-    const int64_t rem = E1 - Eb;
-    const int nvalid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
-    const int col = col_n;
-    const TC a = a_n;
-    if (gb + 1 < ngb) fetch(gb + 1);
-    uint32_t bits = 0u;
-    if (nvalid > 0) bits = (bm[Eb >> 5] >> (Eb & 31)) & 0xFFu;
-    if (gb == 0) bits &= ~1u;
-    bits &= (1u << nvalid) - 1u;
-    __syncwarp();
-    s_col[q] = col;
-    __syncwarp();
-    int cols[8];
-    {
-      const int4 c0 = reinterpret_cast<const int4*>(s_col)[0];
-      const int4 c1 = reinterpret_cast<const int4*>(s_col)[1];
-      cols[0] = c0.x; cols[1] = c0.y; cols[2] = c0.z; cols[3] = c0.w;
-      cols[4] = c1.x; cols[5] = c1.y; cols[6] = c1.z; cols[7] = c1.w;
-    }
-    TS h[8][V];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
-    TC p[8];
-    const int row_b = row;
-    const bool fr_b = first_row;
-    if (bits == 0u) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        TC v = TC(0);
-#pragma unroll
-        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
-        p[i] = v;
-      }
+  // Prefetch ring in shared memory, filled with cp.async one 32-entry block
+  // ahead: per block the group's 32 column ids, row ids and values (8 x 16 B
+  // chunks each; lane q copies chunk q of each stream). The step loop then
+  // needs no unrolling (I-cache) and the ring costs no registers.
+  const int nblk = P.cb / 4;  // warp-uniform
+  constexpr int VPC = 16 / (int)sizeof(TS);  // values per 16-byte chunk
+  auto fetch_block = [&](int b) {
+    if (b * 32 >= nvalid_all) return;  // never read past this worker's end (+pad)
+    const int slot = b & 1;
+    const int o = b * 32;
+    cp_async16(s_ring + slot * 32 + q * 4, pidx - q + o + q * 4);
+    cp_async16(s_ring + 64 + slot * 32 + q * 4, prow - q + o + q * 4);
+    if (VPC == 4) {
+      cp_async16(s_vring + slot * 32 + q * 4, pval - q + o + q * 4);
     } else {
+      cp_async16(s_vring + slot * 32 + q * 4, pval - q + o + q * 4);
+      cp_async16(s_vring + slot * 32 + q * 4 + 2, pval - q + o + q * 4 + 2);
+    }
+  };
+  // zero the ring: inactive workers (padding groups of the last warp) and
+  // blocks past a worker's end must gather valid rows (index 0)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if ((bits >> i) & 1u) {
-          ++rank;
-          row = nzrows[rank];
-          load_w(row);
-          s_rows[i] = row;
-        }
-        TC v = TC(0);
+  for (int z = 0; z < 16; ++z) s_ring[q * 16 + z] = 0;
 #pragma unroll
-        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
-        p[i] = v;
+  for (int z = 0; z < 8; ++z) s_vring[q * 8 + z] = TS(0);
+  __syncwarp();
+  fetch_block(0);
+  cp_async_commit();
+  uint32_t mw_next = nvalid_all > 0 ? pbm[0] : 0u;
+  for (int b = 0; b < nblk; ++b) {
+    fetch_block(b + 1 < nblk ? b + 1 : nblk);
+    cp_async_commit();
+    cp_async_wait<1>();   // block b landed (own copies)
+    __syncwarp();         // ... and the other lanes' copies of this group
+    uint32_t m = mw_next;
+    if (b + 1 < nblk && (b + 1) * 32 < nvalid_all) mw_next = pbm[b + 1];
+    const int left = nvalid_all - b * 32;
+    if (left < 32) m &= left <= 0 ? 0u : ((1u << left) - 1u);
+    if (b == 0) m &= ~1u;
+    const int slot = b & 1;
+    for (int u = 0; u < 4; ++u) {
+      const int o = b * 32 + u * 8;
+      const uint32_t bits = (m >> (8 * u)) & 0xFFu;
+      const bool valid = o + q < nvalid_all;
+      const int* rc = s_ring + slot * 32 + u * 8;        // this group-batch's cols
+      const int* rr = s_ring + 64 + slot * 32 + u * 8;   // ... rows
+      const TC a = (TC)s_vring[slot * 32 + u * 8 + q];
+      int cols[8];
+      {
+        const int4 x0 = reinterpret_cast<const int4*>(rc)[0];
+        const int4 x1 = reinterpret_cast<const int4*>(rc)[1];
+        cols[0] = x0.x; cols[1] = x0.y; cols[2] = x0.z; cols[3] = x0.w;
+        cols[4] = x1.x; cols[5] = x1.y; cols[6] = x1.z; cols[7] = x1.w;
       }
-    }
-    const TC dot = reduce8(p);
-    const bool valid = q < nvalid;
-    const TC r = valid ? dot - a : TC(0);
-    if (valid) {
-      if (P.R) P.R[Eb + q] = (TS)r;
-      if (P.want_sq) sq += (double)r * (double)r;
-    }
-    __syncwarp();
-    s_r[q] = r;
-    __syncwarp();
-    TC r8[8];
-    ld4<TC>(s_r, *reinterpret_cast<TC(*)[4]>(&r8[0]));
-    ld4<TC>(s_r + 4, *reinterpret_cast<TC(*)[4]>(&r8[4]));
-    if (bits == 0u) {
+      TS h[8][V];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
+        ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
+      TC p[8];
+      const int row_b = row;
+      const bool fr_b = first_row;
+      if (bits == 0u) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
-    } else {
-      int rw = row_b;
-      bool fr = fr_b;
+        for (int i = 0; i < 8; ++i) {
+          TC v = TC(0);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if ((bits >> i) & 1u) {
-          flush(rw, fr, false);
-          fr = false;
-          rw = s_rows[i];
-#pragma unroll
-          for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
+          for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
+          p[i] = v;
         }
+      } else {
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+        for (int i = 0; i < 8; ++i) {
+          if ((bits >> i) & 1u) {
+            row = rr[i];
+            load_w(row);
+          }
+          TC v = TC(0);
+#pragma unroll
+          for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
+          p[i] = v;
+        }
       }
-      first_row = fr;
+      const TC dot = reduce8(p);
+      const TC r = valid ? dot - a : TC(0);
+      if (valid) {
+        if (P.R) P.R[E0 + o + q] = (TS)r;
+        sq += (double)r * (double)r;
+      }
+      __syncwarp();
+      s_r[q] = r;
+      __syncwarp();
+      TC r8[8];
+      ld4<TC>(s_r, *reinterpret_cast<TC(*)[4]>(&r8[0]));
+      ld4<TC>(s_r + 4, *reinterpret_cast<TC(*)[4]>(&r8[4]));
+      if (bits == 0u) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+      } else {
+        int rw = row_b;
+        bool fr = fr_b;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if ((bits >> i) & 1u) {
+            flush(rw, fr, false);
+            fr = false;
+            rw = rr[i];
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
+          }
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+        }
+        first_row = fr;
+      }
     }
+  }
+  cp_async_wait<0>();
+  if (P.probe) {
+    asm volatile("" ::"f"((float)acc.a[0]));
+    t_loop = clock64();
   }
   if (active) {
     flush(row, first_row, true);
-    if (q == 0) {
+    if (q == 0 && !P.row_cnt) {
       P.carry_row[2 * chunk] = row_first;
       P.carry_row[2 * chunk + 1] = row_last;
     }
+  }
+  if (P.row_cnt) {
+    // Deferred crossing notification: one release fence per warp (MEMBAR.GPU,
+    // no L1 invalidation) orders all carry stores of its groups before their
+    // counter increments; the worker depositing a row's last piece finishes
+    // it. The finisher reads the pieces through L2 (ld.cg) after its own
+    // increment returned, so it observes every earlier piece.
+    __syncwarp();
+    const bool any = __any_sync(0xffffffffu, row_first >= 0 || row_last >= 0);
+    if (any) {
+      if ((threadIdx.x & 31) == 0) asm volatile("fence.release.gpu;" ::: "memory");
+      __syncwarp();
+      const int64_t CB64 = CB;
+      if (row_first >= 0)
+        finish_row<TS, TC, V>(P.out, P.ldout, P.out_scale, P.carry_vec, P.row_cnt, P.lay.ptr,
+                              CB64, k, kp, row_first);
+      if (row_last >= 0)
+        finish_row<TS, TC, V>(P.out, P.ldout, P.out_scale, P.carry_vec, P.row_cnt, P.lay.ptr,
+                              CB64, k, kp, row_last);
+    }
+  }
+  if (P.probe && active && q == 0) {
+    long long* pr = P.probe + 10 * (int64_t)chunk;
+    pr[0] = t_start;
+    pr[1] = t_init;
+    pr[2] = t_loop;
+    pr[3] = clock64();
   }
   if (P.part) {
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
     if (q == 0 && chunk < P.nchunks) {
-      P.part[chunk] = sq;
+      P.part[chunk] = P.want_sq ? sq : 0.0;
       P.part[P.nchunks + chunk] = 0.0;
       P.part[2 * P.nchunks + chunk] = 0.0;
     }
   }
 }
 
-template <typename TS, typename TC, int V>
-__global__ void __launch_bounds__(kThreads)
-k_sweep_g8(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp) {
-  __shared__ __align__(16) int32_t s_col[kThreads / 8][8];
-  __shared__ __align__(16) TC s_r[kThreads / 8][8];
-  __shared__ int32_t s_rows[kThreads / 8][8];
-  const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;  // global group id
-  const int wbase = gid & ~3;                                     // first group of this warp
-  if (wbase >= ntot) return;                                      // warp-uniform
-  const int gl = threadIdx.x >> 3;
-  if (wbase < n0p) run_group<TS, TC, V>(P0, gid, k, kp, s_col[gl], s_r[gl], s_rows[gl]);
-  else run_group<TS, TC, V>(P1, gid - n0p, k, kp, s_col[gl], s_r[gl], s_rows[gl]);
-}
-
-// Epilogue: carries, empty rows, deterministic reductions.
 struct SumJob {
   const double* part;  // [3][np]
   int np;
@@ -812,39 +934,42 @@ struct SumJob {
   double* sums;        // [5] out: sq, s1, s2, |W|^2, |H|^2 (first 3 used by callers)
 };
 
+// One warp per head slot. Heads are the used odd slots (a row's last
+// chunk-crossing); the run of slots carrying the same row follows in slot
+// order (unused slots = -1), and is summed in that fixed order.
 template <typename TS, typename TC>
-__device__ void carry_fixup(const Pass<TS, TC>& P, int k, int warp_global, int nwarps_grid) {
+__device__ void carry_head(const Pass<TS, TC>& P, int k, int q) {
   const int lane = lane_id();
   const int nslots = 2 * P.nchunks;
   const int cs = P.cstride;
-  // Heads are the used odd slots (a row's last chunk-crossing); the run of
-  // slots carrying the same row follows in slot order (unused slots = -1).
-  for (int q = 2 * warp_global + 1; q < nslots; q += 2 * nwarps_grid) {
-    const int row = P.carry_row[q];
-    if (row < 0) continue;
-    // find the run end with a warp-wide scan of the next 32 slots at a time
-    int end = q + 1;
-    while (end < nslots) {
-      const int sidx = end + lane;
-      const int r2 = sidx < nslots ? P.carry_row[sidx] : -2;
-      const bool stop = (sidx >= nslots) || (r2 >= 0 && r2 != row);
-      const unsigned b = __ballot_sync(0xffffffffu, stop);
-      if (b) { end += __ffs(b) - 1; break; }
-      end += 32;
-    }
-    if (end > nslots) end = nslots;
-    for (int d0 = 0; d0 < k; d0 += 32) {
-      const int d = d0 + lane;
-      TC v = TC(0);
-      if (d < k) {
+  const int row = P.carry_row[q];
+  if (row < 0) return;
+  int end = q + 1;
+  while (end < nslots) {
+    const int sidx = end + lane;
+    const int r2 = sidx < nslots ? P.carry_row[sidx] : -2;
+    const bool stop = (sidx >= nslots) || (r2 >= 0 && r2 != row);
+    const unsigned b = __ballot_sync(0xffffffffu, stop);
+    if (b) { end += __ffs(b) - 1; break; }
+    end += 32;
+  }
+  if (end > nslots) end = nslots;
+  for (int d0 = 0; d0 < k; d0 += 32) {
+    const int d = d0 + lane;
+    TC v = TC(0);
+    if (d < k) {
 #pragma unroll 4
-        for (int sl = q; sl < end; ++sl) {
-          if (P.carry_row[sl] == row) v += P.carry_vec[(int64_t)sl * cs + d];
-        }
-        P.out[(int64_t)row * P.ldout + d] = (TS)(v * (TC)P.out_scale);
+      for (int sl = q; sl < end; ++sl) {
+        if (P.carry_row[sl] == row) v += P.carry_vec[(int64_t)sl * cs + d];
       }
+      P.out[(int64_t)row * P.ldout + d] = (TS)(v * (TC)P.out_scale);
     }
   }
+}
+
+template <typename TS, typename TC>
+__device__ void empty_rows_zero(const Pass<TS, TC>& P, int k, int warp_global, int nwarps_grid) {
+  const int lane = lane_id();
   for (int i = warp_global; i < P.lay.n_empty; i += nwarps_grid) {
     const int row2 = P.lay.empty_rows[i];
     for (int d = lane; d < k; d += 32) P.out[(int64_t)row2 * P.ldout + d] = TS(0);
@@ -860,26 +985,32 @@ __global__ void __launch_bounds__(256)
 k_epilogue(Pass<TS, TC> P0, int has0, Pass<TS, TC> P1, int has1, int k, SumJob J) {
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwg = (gridDim.x * blockDim.x) >> 5;
-  if (has0 && P0.out) carry_fixup(P0, k, wg, nwg);
-  if (has1 && P1.out) carry_fixup(P1, k, wg, nwg);
+  // carries: warp wg owns head slot 2*wg+1 of each pass (grid sized for it)
+  if (has0 && P0.out) {
+    for (int q = 2 * wg + 1; q < 2 * P0.nchunks; q += 2 * nwg) carry_head(P0, k, q);
+    empty_rows_zero(P0, k, wg, nwg);
+  }
+  if (has1 && P1.out) {
+    for (int q = 2 * wg + 1; q < 2 * P1.nchunks; q += 2 * nwg) carry_head(P1, k, q);
+    empty_rows_zero(P1, k, wg, nwg);
+  }
   if (!J.block_part) return;
-  // per-block partials over fixed slices
   __shared__ double sm[8];
   double v[5] = {0, 0, 0, 0, 0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < J.np; i += gridDim.x * blockDim.x) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < J.np; i += nth) {
     v[0] += J.part[i];
     v[1] += J.part[J.np + i];
     v[2] += J.part[2 * J.np + i];
   }
   if (J.W)
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < J.wcount;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = tid; i < J.wcount; i += nth) {
       const double x = ldv(J.W, i, J.is_f64);
       v[3] += x * x;
     }
   if (J.H)
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < J.hcount;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = tid; i < J.hcount; i += nth) {
       const double x = ldv(J.H, i, J.is_f64);
       v[4] += x * x;
     }
@@ -908,7 +1039,119 @@ k_epilogue(Pass<TS, TC> P0, int has0, Pass<TS, TC> P1, int has1, int k, SumJob J
   }
 }
 
-constexpr int kEpiBlocks = 2 * kNumSMs;
+struct FusedRed {
+  const void* W;
+  int64_t wcount;
+  const void* H;
+  int64_t hcount;
+  int is_f64;
+  double* block_part;    // [gridDim.x][3]
+  unsigned int* counter; // zero at rest (the last block re-zeroes it)
+  double* sums;          // out: sum r^2, |W|^2, |H|^2
+};
+
+__device__ __forceinline__ double ldv2(const void* p, int64_t i, int is_f64) {
+  return is_f64 ? static_cast<const double*>(p)[i] : (double)static_cast<const float*>(p)[i];
+}
+
+template <typename TS, typename TC, int V>
+__global__ void __launch_bounds__(kThreads, (V <= 4 && sizeof(TC) == 4) ? MFG_G8_MINB : 1)
+k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, FusedRed F) {
+  __shared__ __align__(16) int32_t s_ring[kThreads / 8][128];   // [cols|rows][2 slots][32]
+  __shared__ __align__(16) TS s_vring[kThreads / 8][64];        // [2 slots][32]
+  __shared__ __align__(16) TC s_r[kThreads / 8][8];
+  const int lane = threadIdx.x & 31;
+  const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;
+  const int wbase = gid & ~3;
+  const int gl = threadIdx.x >> 3;
+  if (wbase < ntot) {  // warp-uniform
+    // one inlined copy of the worker (I-cache): select the orientation's pass
+    const bool second = wbase >= n0p;
+    const Pass<TS, TC>& P = second ? P1 : P0;
+    run_group<TS, TC, V>(P, second ? gid - n0p : gid, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
+  }
+  const int wg = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int nwg = (gridDim.x * kThreads) >> 5;
+  empty_rows_zero(P0, k, wg, nwg);
+  empty_rows_zero(P1, k, wg, nwg);
+  // per-warp fp64 partials of the dense norms (fixed slices), then a
+  // barrier-free two-level last-arriver reduction: the last warp of each
+  // block folds its block's warp partials, the last block folds the blocks.
+  const int64_t gl0 = (int64_t)wg * 32 + lane, gstride = (int64_t)nwg * 32;
+  double w2 = 0.0, h2 = 0.0;
+  for (int64_t i = gl0; i < F.wcount; i += gstride) { const double x = ldv2(F.W, i, F.is_f64); w2 += x * x; }
+  for (int64_t i = gl0; i < F.hcount; i += gstride) { const double x = ldv2(F.H, i, F.is_f64); h2 += x * x; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+    h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+  }
+  double* wp = F.block_part;                       // [nwg][2] warp partials
+  double* bp = F.block_part + 2 * (int64_t)nwg;    // [gridDim.x][3] block partials
+  unsigned int* bcnt = F.counter + 1;              // [gridDim.x] per-block counters
+  const int wib = threadIdx.x >> 5;
+  bool last_w = false;
+  if (lane == 0) {
+    wp[2 * wg] = w2;
+    wp[2 * wg + 1] = h2;
+    asm volatile("fence.release.gpu;" ::: "memory");
+    last_w = atomicAdd(&bcnt[blockIdx.x], 1u) == kThreads / 32 - 1;
+  }
+  last_w = __shfl_sync(0xffffffffu, last_w, 0);
+  if (!last_w) return;
+  // last warp of this block: fold the block's warp partials (fixed order)
+  double t1 = 0.0, t2 = 0.0;
+  if (lane < kThreads / 32) {
+    const int w = blockIdx.x * (kThreads / 32) + lane;
+    t1 = __ldcg(wp + 2 * w);
+    t2 = __ldcg(wp + 2 * w + 1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+  }
+  bool last_b = false;
+  if (lane == 0) {
+    bcnt[blockIdx.x] = 0u;
+    bp[3 * blockIdx.x + 1] = t1;
+    bp[3 * blockIdx.x + 2] = t2;
+    asm volatile("fence.release.gpu;" ::: "memory");
+    last_b = atomicAdd(F.counter, 1u) == gridDim.x - 1;
+  }
+  last_b = __shfl_sync(0xffffffffu, last_b, 0);
+  if (!last_b) return;
+  (void)wib;
+  // last block's last warp: fold block partials and the chunk sum r^2
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  for (int64_t i = lane; i < P0.nchunks; i += 32) u0 += __ldcg(P0.part + i);
+  for (unsigned int b2 = lane; b2 < gridDim.x; b2 += 32) {
+    u1 += __ldcg(bp + 3 * b2 + 1);
+    u2 += __ldcg(bp + 3 * b2 + 2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    u0 += __shfl_xor_sync(0xffffffffu, u0, o);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, o);
+    u2 += __shfl_xor_sync(0xffffffffu, u2, o);
+  }
+  if (lane == 0) {
+    F.sums[0] = u0;
+    F.sums[1] = u1;
+    F.sums[2] = u2;
+    *F.counter = 0u;
+  }
+}
+
+constexpr int kEpiBlocksMax = 32 * kNumSMs;
+
+int epi_blocks(int nch0, int nch1) {
+  const int heads = nch0 > nch1 ? nch0 : nch1;
+  int b = (heads + 7) / 8;
+  if (b < 2 * kNumSMs) b = 2 * kNumSMs;
+  if (b > kEpiBlocksMax) b = kEpiBlocksMax;
+  return b;
+}
 
 int pick_cb(int64_t nnz) {
   // target >= ~16 warps per SM of chunks, batches in [2, 32]
@@ -930,11 +1173,18 @@ int grouped_kp(int k, int elem_bytes) {
 }
 
 int pick_cb_g(int64_t nnz) {
-  const int64_t target = (int64_t)kNumSMs * 96;  // ~24 warps x 4 groups per SM
+  // Target worker count per orientation (default: one resident wave for both
+  // passes, 16 warps x 4 groups per SM). Longer chunks amortise the
+  // per-worker fixed costs (schedule lookup chain, crossing-row notification).
+  static const int64_t env_target = [] {
+    const char* e = getenv("MFG_WORKERS_PER_SM");
+    return e ? (int64_t)atoi(e) : (int64_t)32;
+  }();
+  const int64_t target = (int64_t)kNumSMs * env_target;
   int64_t cb = (nnz + 8 * target - 1) / (8 * target);
   if (cb < 4) cb = 4;
-  if (cb > 256) cb = 256;
-  return (int)cb;
+  if (cb > 512) cb = 512;
+  return (int)((cb + 3) & ~3);
 }
 
 int chunks_of_g(int64_t nnz, int cb) {
@@ -960,7 +1210,7 @@ void carve_pass(C& c, const mfg_layout* lay, int k, bool acc, bool part) {
 
 template <typename C>
 void carve_epi(C& c) {
-  c.template take<double>((size_t)kEpiBlocks * 5);
+  c.template take<double>((size_t)kEpiBlocksMax * 5);
   c.template take<unsigned int>(1);
   c.template take<double>(5);
 }
@@ -990,25 +1240,31 @@ bool setup_pass(Pass<TS, TC>& P, Carver& c, const mfg_layout* lay, int k, bool a
   return c.ok;
 }
 
+
+int grouped_grid(int n0, int n1) {
+  const int ntot = ((n0 + 3) & ~3) + ((n1 + 3) & ~3);
+  int g = (ntot + kThreads / 8 - 1) / (kThreads / 8);
+  return g < 1 ? 1 : g;
+}
+
 template <typename TS, typename TC>
 int launch_grouped(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k, int kp,
-                   cudaStream_t stream) {
+                   const FusedRed& F, cudaStream_t stream) {
   const int n0p = (P0.nchunks + 3) & ~3;
   const int n1p = (P1.nchunks + 3) & ~3;
   const int ntot = n0p + n1p;
-  if (ntot == 0) return MFG_OK;
-  const int groups_per_block = kThreads / 8;
-  const int grid = (ntot + groups_per_block - 1) / groups_per_block;
+  const int grid = grouped_grid(P0.nchunks, P1.nchunks);
   const int V = kp / 8;
   constexpr bool f32 = sizeof(TS) == 4, mixed = sizeof(TS) != sizeof(TC);
+  auto go = [&](auto kern) { kern<<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp, F); };
   if constexpr (f32 && !mixed) {
-    if (V == 4) k_sweep_g8<TS, TC, 4><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
-    else k_sweep_g8<TS, TC, 8><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+    if (V == 4) go(k_sweep_g8f<TS, TC, 4>);
+    else go(k_sweep_g8f<TS, TC, 8>);
   } else if constexpr (f32) {
-    k_sweep_g8<TS, TC, 4><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+    go(k_sweep_g8f<TS, TC, 4>);
   } else {
-    if (V == 2) k_sweep_g8<TS, TC, 2><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
-    else k_sweep_g8<TS, TC, 4><<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp);
+    if (V == 2) go(k_sweep_g8f<TS, TC, 2>);
+    else go(k_sweep_g8f<TS, TC, 4>);
   }
   MFG_LAUNCH_CHECK();
   return MFG_OK;
@@ -1043,6 +1299,12 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
              void* RH, void* RtW, double out_scale, double* sums, void* ws, size_t wsb,
              cudaStream_t stream) {
   Carver c(ws, wsb);
+  // persistent, zero-at-rest state first (fixed offsets for every path)
+  int32_t* cnt0 = c.take<int32_t>((size_t)csr->nrows + 1);
+  int32_t* cnt1 = c.take<int32_t>((size_t)csc->nrows + 1);
+  const int ggrid = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
+                                 chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
+  unsigned int* fcounter = c.take<unsigned int>((size_t)ggrid + 1);
   Pass<TS, TC> P0{}, P1{};
   const bool acc0 = RH != nullptr, acc1 = RtW != nullptr;
   // grouped v3 kernel: zero-padded factors of width kp, all outputs wanted
@@ -1059,7 +1321,10 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
     P1.scale = nullptr; P1.other = (const TS*)W; P1.ldo = ldw; P1.R = nullptr; P1.r_mult = 1.0;
     P1.out = (TS*)RtW; P1.ldout = k; P1.out_scale = out_scale; P1.want_sq = 0;
     SumJob J{};
-    J.block_part = c.take<double>((size_t)kEpiBlocks * 5);
+    {
+      const size_t gb = grouped ? (size_t)grouped_grid(P0.nchunks, P1.nchunks) * (3 + 2 * (kThreads / 32)) : 0;
+      J.block_part = c.take<double>(gb > (size_t)kEpiBlocksMax * 5 ? gb : (size_t)kEpiBlocksMax * 5);
+    }
     J.counter = c.take<unsigned int>(1);
     double* tmp = c.take<double>(5);
     if (!c.ok) goto small;
@@ -1070,14 +1335,31 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
     J.is_f64 = sizeof(TS) == 8;
     J.sums = tmp;
     if (ldw < k || ldh < k) { set_error("sweep requires ldw, ldh >= k"); return MFG_ERR_ARG; }
-    // counter must start at zero: the epilogue's last block re-zeroes it.
-    MFG_CUDA_CHECK(cudaMemsetAsync(J.counter, 0, sizeof(unsigned int), stream));
     const int n0 = csr->nnz ? P0.nchunks : 0;
     const int n1 = (acc1 && csc->nnz) ? P1.nchunks : 0;
     int st;
+    // counter must start at zero: the epilogue's last block re-zeroes it.
+    if (!grouped) MFG_CUDA_CHECK(cudaMemsetAsync(J.counter, 0, sizeof(unsigned int), stream));
     prof_begin(stream);
-    if (grouped) st = launch_grouped<TS, TC>(P0, P1, k, kpg, stream);
-    else if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
+    if (grouped) {
+      P0.row_cnt = cnt0;
+      P1.row_cnt = cnt1;
+      P0.probe = P1.probe = nullptr;
+      if (g_probe) {
+        P0.probe = g_probe;
+        P1.probe = g_probe + 10 * (int64_t)P0.nchunks;
+      }
+      FusedRed F{};
+      F.W = W; F.wcount = J.wcount; F.H = H; F.hcount = J.hcount; F.is_f64 = J.is_f64;
+      F.block_part = J.block_part; F.counter = fcounter; F.sums = tmp;
+      st = launch_grouped<TS, TC>(P0, P1, k, kpg, F, stream);
+      prof_end(stream);
+      if (st != MFG_OK) return st;
+      MFG_CUDA_CHECK(cudaMemcpyAsync(sums, tmp, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     stream));
+      return MFG_OK;
+    }
+    if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
     else st = launch_main<TS, TC, false>(P0, P1, n0, 0, k, stream);
     prof_end(stream);
     if (st != MFG_OK) return st;
@@ -1085,7 +1367,8 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
       MFG_CUDA_CHECK(cudaMemsetAsync(P0.part, 0, sizeof(double) * 3, stream));
       J.np = 1;
     }
-    k_epilogue<TS, TC><<<kEpiBlocks, 256, 0, stream>>>(P0, acc0 ? 1 : 0, P1, acc1 ? 1 : 0, k, J);
+    k_epilogue<TS, TC><<<epi_blocks(acc0 ? P0.nchunks : 0, acc1 ? P1.nchunks : 0), 256, 0, stream>>>(
+        P0, acc0 ? 1 : 0, P1, acc1 ? 1 : 0, k, J);
     MFG_LAUNCH_CHECK();
     // sums = [sq, |W|^2, |H|^2]
     MFG_CUDA_CHECK(cudaMemcpyAsync(sums, tmp, sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -1112,7 +1395,7 @@ int do_sddmm(const mfg_layout* lay, int k, const void* L, int ldl, const double*
   P.other = (const TS*)Rt; P.ldo = ldr; P.R = (TS*)out; P.r_mult = out_mult; P.out = nullptr;
   P.ldout = 0; P.out_scale = 1.0; P.want_sq = 1;
   SumJob J{};
-  J.block_part = c.take<double>((size_t)kEpiBlocks * 5);
+  J.block_part = c.take<double>((size_t)kEpiBlocksMax * 5);
   J.counter = c.take<unsigned int>(1);
   double* tmp = c.take<double>(5);
   if (!c.ok) {
@@ -1128,7 +1411,7 @@ int do_sddmm(const mfg_layout* lay, int k, const void* L, int ldl, const double*
     MFG_CUDA_CHECK(cudaMemsetAsync(P.part, 0, sizeof(double) * 3, stream));
     J.np = 1;
   }
-  k_epilogue<TS, TC><<<kEpiBlocks, 256, 0, stream>>>(P, 0, P, 0, k, J);
+  k_epilogue<TS, TC><<<2 * kNumSMs, 256, 0, stream>>>(P, 0, P, 0, k, J);
   MFG_LAUNCH_CHECK();
   if (sums)
     MFG_CUDA_CHECK(cudaMemcpyAsync(sums, tmp, 3 * sizeof(double), cudaMemcpyDeviceToDevice, stream));
@@ -1139,9 +1422,17 @@ int do_sddmm(const mfg_layout* lay, int k, const void* L, int ldl, const double*
 
 size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
   Sizer s;
+  s.take<int32_t>((size_t)csr->nrows + 1);
+  s.take<int32_t>((size_t)csc->nrows + 1);
+  const int64_t gg = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
+                                  chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
+  s.take<unsigned int>((size_t)gg + 1);
   carve_pass(s, csr, k, true, true);
   carve_pass(s, csc, k, true, false);
   carve_epi(s);
+  const int64_t g = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
+                                 chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
+  s.take<double>((size_t)g * (3 + 2 * (kThreads / 32)));
   return s.off + 1024;
 }
 
@@ -1212,5 +1503,10 @@ extern "C" int mfg_profile_collect(double* total_ms, int* count) {
   *total_ms = t;
   *count = (int)g_prof.used;
   g_prof.used = 0;
+  return MFG_OK;
+}
+
+extern "C" int mfg_set_probe(void* dev_buffer) {
+  mfg::g_probe = static_cast<long long*>(dev_buffer);
   return MFG_OK;
 }

@@ -48,6 +48,22 @@ def _i32(n):
     return torch.empty(max(int(n), 0), dtype=torch.int32, device="cuda")
 
 
+# Entry-stream arrays (column / row indices, values) are allocated with
+# OMEGA_PAD zero entries past nnz: the grouped sweep kernel prefetches a
+# block ahead without bounds guards (include/mfg_b200.h).
+OMEGA_PAD = 64
+
+
+def _padded(n, dtype, device="cuda"):
+    return torch.zeros(max(int(n), 0) + OMEGA_PAD, dtype=dtype, device=device)[: max(int(n), 0)]
+
+
+def _padded_copy(t):
+    out = _padded(t.numel(), t.dtype, t.device)
+    out.copy_(t)
+    return out
+
+
 class _LayoutBuffers:
     """One orientation's device arrays + its ctypes ``mfg_layout``."""
 
@@ -97,13 +113,13 @@ class OmegaDevice:
         self.nnz = nnz
         dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
-        rows = _i32(nnz)
-        cols = _i32(nnz)
-        vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+        rows = _padded(nnz, torch.int32, dev)
+        cols = _padded(nnz, torch.int32, dev)
+        vals = _padded(nnz, torch.float64, dev)
         ptr = _i32(self.m + 1)
         csc_ptr = _i32(self.n + 1)
-        csc_rows = _i32(nnz)
-        csc_cols = _i32(nnz)
+        csc_rows = _padded(nnz, torch.int32, dev)
+        csc_cols = _padded(nnz, torch.int32, dev)
         csc_perm = _i32(nnz)
         wsb = lib.mfg_omega_build_workspace(nnz, self.m, self.n)
         ws = _lib.WS.get(wsb, dev)
@@ -126,7 +142,7 @@ class OmegaDevice:
             raise DatasetError(f"duplicate entry at ({r}, {c}); refusing to aggregate")
         _lib.check(st, "omega build")
         self.vals64 = vals
-        self.vals = vals if dtype == torch.float64 else vals.to(dtype)
+        self.vals = vals if dtype == torch.float64 else _padded_copy(vals.to(dtype))
         self.csr = _LayoutBuffers(self.m, self.n, nnz, ptr, cols, rows)
         self.csc = _LayoutBuffers(self.n, self.m, nnz, csc_ptr, csc_rows, csc_cols)
         self.csc_perm = csc_perm
@@ -134,7 +150,7 @@ class OmegaDevice:
 
     def gather_csc(self, vals: torch.Tensor) -> torch.Tensor:
         """Values in CSR order -> CSC order (one gather kernel)."""
-        out = torch.empty_like(vals)
+        out = _padded(vals.numel(), vals.dtype, vals.device)
         _lib.check(_lib.lib().mfg_gather(_lib.dtype_code(vals.dtype), self.nnz,
                                          self.csc_perm.data_ptr(), vals.data_ptr(),
                                          out.data_ptr(), _lib.stream_ptr()), "gather")
@@ -222,7 +238,7 @@ class ObservationSet:
         d = object.__new__(OmegaDevice)
         d.__dict__.update(self.dev.__dict__)
         d.dtype = dtype
-        d.vals = self.dev.vals64 if dtype == torch.float64 else self.dev.vals64.to(dtype)
+        d.vals = self.dev.vals64 if dtype == torch.float64 else _padded_copy(self.dev.vals64.to(dtype))
         d.vals_csc = self.dev.gather_csc(d.vals)
         return ObservationSet(self.m, self.n, d, self.transposed, self.row_ids, self.col_ids)
 

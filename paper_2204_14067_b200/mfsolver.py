@@ -82,7 +82,8 @@ class SweepPlan:
         self.sums = torch.zeros(3, dtype=torch.float64, device=dev.device)
         lib = _lib.lib()
         self.wsb = lib.mfg_sweep_workspace(dev.csr.ref, dev.csc.ref, max(self.k, 1))
-        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=dev.device)
+        # zero-filled once: the grouped kernel keeps zero-at-rest counters here
+        self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
         self.kp = grouped_width(self.k, dt, compute_f64)
 
     def pad(self, f: torch.Tensor) -> torch.Tensor:
