@@ -65,11 +65,11 @@ def instance(workload: str, seed: int):
 
 
 def kernel_bytes(nnz: int, m: int, n: int, k: int, s_v: int) -> int:
-    """Compulsory DRAM bytes of one fused sweep launch:
-    CSR pass reads idx+A, writes R; CSC pass reads idx+A; 8 B of schedule
-    metadata per 32 entries per pass; W and H read once and RH, RtW written
-    once (s_v bytes per value)."""
-    per_nnz = 4 + s_v + s_v + 4 + s_v + 0.5
+    """Compulsory DRAM bytes of one grouped sweep launch:
+    CSR pass reads column ids, row ids and A and writes R; CSC pass reads row
+    ids, column ids and A; 4 B of schedule mask per 32 entries per pass; W
+    and H read once and RH, RtW written once (s_v bytes per value)."""
+    per_nnz = (4 + 4 + s_v + s_v) + (4 + 4 + s_v) + 0.25
     return int(nnz * per_nnz + 3 * s_v * (m + n) * k)
 
 
@@ -181,7 +181,7 @@ def run_reference(args, rank, world):
     el = time.perf_counter() - t0
     value = args.steps / el
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
