@@ -1,0 +1,142 @@
+"""Multi-rank path on CPU: world_size 2 over gloo with the
+oracle as local arithmetic, checked against the single-process oracle; plus
+a 1-GPU emulation of the 2-shard decomposition on the CUDA kernels."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import mfg_oracle as orc
+from paper_2204_14067_b200 import sharding, synth
+
+
+class OracleOps:
+    """Local arithmetic of ShardedMF restated on the CPU oracle (test only)."""
+
+    def prepare(self, nrows, ncols, rows, cols, vals):
+        return orc.from_coo(nrows, ncols, rows, cols, vals)
+
+    def sweep(self, om, self_rows, other_full):
+        w, h = self_rows.numpy(), other_full.numpy()
+        r = orc.residual(om, w, h)
+        return torch.as_tensor(orc.spmm_csr(om, r, h)), float(r @ r)
+
+    def half_sweep(self, om, other_full, lam):
+        o = other_full.numpy()
+        return torch.as_tensor(orc.half_sweep(om.a_csr, om.pattern_csr, o, lam))
+
+
+def _instance():
+    m, n, r, c, v = synth.generate("c2", scale=0.05, seed=11)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    w, h = synth.sweep_factors(m, n, 6, seed=3)
+    return m, n, r, c, v, w, h
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, n, r, c, v, w, h = _instance()
+        shard = sharding.make_shard(m, n, r, c, v, rank, world)
+        mf = sharding.ShardedMF(shard, OracleOps(), sharding.Comm(), torch.device("cpu"))
+        W, H = torch.as_tensor(w), torch.as_tensor(h)
+        rh, rtw, sq = mf.sweep(W, H)
+        obj = mf.objective(W, H, 3.0)
+        w1, h1 = mf.bcd_epoch(W, H, 3.0)
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), rh=rh.numpy(), rtw=rtw.numpy(), sq=sq,
+                 obj=obj, w1=w1.numpy(), h1=h1.numpy(),
+                 rb=np.array(shard.row_block), cb=np.array(shard.col_block))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_balanced_blocks_cover_and_balance():
+    counts = np.array([100, 1, 1, 1, 50, 50, 0, 0, 3, 200, 1, 1])
+    for parts in (1, 2, 3, 5):
+        b = sharding.balanced_blocks(counts, parts)
+        assert b[0][0] == 0 and b[-1][1] == counts.size
+        assert all(b[i][1] == b[i + 1][0] for i in range(parts - 1))
+    b = sharding.balanced_blocks(np.ones(1000, dtype=int), 4)
+    assert [y - x for x, y in b] == [250, 250, 250, 250]
+
+
+def test_make_shard_partitions_omega():
+    m, n, r, c, v, _, _ = _instance()
+    seen_r, seen_c = 0, 0
+    for rank in range(3):
+        s = sharding.make_shard(m, n, r, c, v, rank, 3)
+        seen_r += s.r_vals.size
+        seen_c += s.c_vals.size
+        assert np.all(s.r_rows >= 0) and np.all(s.r_rows < s.row_block[1] - s.row_block[0])
+        assert np.all(s.c_rows >= 0) and np.all(s.c_rows < s.col_block[1] - s.col_block[0])
+    assert seen_r == v.size and seen_c == v.size
+
+
+def test_two_ranks_gloo_match_single_process():
+    m, n, r, c, v, w, h = _instance()
+    om = orc.from_coo(m, n, r, c, v)
+    rr, rh, rtw, sq, w2, h2 = orc.sweep(om, w, h)
+    w1, h1 = orc.bcd_epoch(om, w, h, 3.0)
+    obj = orc.mf_objective(om, w, h, 3.0)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [np.load(os.path.join(d, f"r{p}.npz")) for p in range(2)]
+    for x in res:
+        # CSR/CSC SpMM rows: each row's sum is computed exactly as unsharded
+        assert np.array_equal(x["rh"], rh)
+        assert np.array_equal(x["rtw"], rtw)
+        assert float(x["sq"]) == pytest.approx(sq, rel=1e-13)
+        assert float(x["obj"]) == pytest.approx(obj, rel=1e-13)
+        # BCD rows are independent exact minimisers: bitwise identical
+        assert np.array_equal(x["w1"], w1)
+        assert np.array_equal(x["h1"], h1)
+    # both ranks hold identical replicas and identical fp64 sums
+    assert float(res[0]["sq"]) == float(res[1]["sq"])
+    assert np.array_equal(res[0]["w1"], res[1]["w1"])
+
+
+@pytest.mark.gpu
+def test_two_shard_decomposition_on_gpu():
+    """The 2-rank decomposition evaluated on one GPU (ranks emulated in turn,
+    collectives replaced by concatenation): equals the unsharded kernels."""
+    from paper_2204_14067_b200 import mfsolver as MF
+    from paper_2204_14067_b200.data import ObservationSet
+    from paper_2204_14067_b200.operators import FactorPair
+
+    m, n, r, c, v, w, h = _instance()
+    W, H = torch.as_tensor(w).cuda(), torch.as_tensor(h).cuda()
+    ops = sharding.DeviceOps(torch.float64)
+    rh_parts, rtw_parts, sqs, w1_parts = [], [], [], []
+    shards = [sharding.make_shard(m, n, r, c, v, p, 2) for p in range(2)]
+    for s in shards:
+        hr = ops.prepare(s.row_block[1] - s.row_block[0], n, s.r_rows, s.r_cols, s.r_vals)
+        hc = ops.prepare(s.col_block[1] - s.col_block[0], m, s.c_rows, s.c_cols, s.c_vals)
+        a, sq = ops.sweep(hr, W[s.row_block[0]:s.row_block[1]], H)
+        b, _ = ops.sweep(hc, H[s.col_block[0]:s.col_block[1]], W)
+        rh_parts.append(a)
+        rtw_parts.append(b)
+        sqs.append(sq)
+        w1_parts.append(ops.half_sweep(hr, H, 3.0))
+    obs = ObservationSet.from_coo(m, n, r, c, v)
+    _, RH, RtW, sums = MF.sweep(obs, FactorPair(W, H), want_rh=True, want_rtw=True)
+    assert torch.allclose(torch.cat(rh_parts), RH, rtol=0, atol=1e-12)
+    assert torch.allclose(torch.cat(rtw_parts), RtW, rtol=0, atol=1e-12)
+    assert sum(sqs) == pytest.approx(float(sums[0]), rel=1e-12)
+    w1 = MF.bcd_epoch(obs, FactorPair(W, H), 3.0).w
+    assert torch.equal(torch.cat(w1_parts), w1)
