@@ -698,9 +698,16 @@ __device__ __noinline__ void finish_row(TS* out, int ldout, double out_scale, TC
 // CB is a multiple of 32 entries; idx / row_of / vals are readable up to
 // nnz + 64 entries (the Omega arrays are allocated with that padding), so
 // the prefetch loads need no bounds guards. Entry offsets are 32-bit.
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Returns the group's fp64 sum r^2 (all 8 lanes hold it; 0 unless want_sq).
 template <typename TS, typename TC, int V>
-__device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int k, int kp,
-                                          int32_t* s_ring, TS* s_vring, TC* s_r) {
+__device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, int k, int kp,
+                                            int32_t* s_ring, TS* s_vring, TC* s_r) {
   const int q = threadIdx.x & 7;
   const int nnz = (int)P.lay.nnz;
   const int CB = P.cb * 8;
@@ -717,7 +724,7 @@ __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int 
   const int nvalid_all = E1 - E0;  // entries of this worker
   bool start_cross = false, end_cross = false;
   int row = 0;
-  long long t_start = clock64();
+  long long t_start = gtimer();
   if (active) {
     start_cross = (pbm[0] & 1u) == 0u;
     row = P.lay.row_of[E0];
@@ -740,7 +747,7 @@ __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int 
   long long t_init = 0, t_loop = 0;
   if (P.probe) {
     asm volatile("" ::"f"((float)w[0]));
-    t_init = clock64();
+    t_init = gtimer();
   }
   AccV<TC, V> acc;
 #pragma unroll
@@ -812,69 +819,69 @@ __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int 
       for (int i = 0; i < 8; ++i)
         ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
       TC p[8];
-      const int row_b = row;
-      const bool fr_b = first_row;
-      if (bits == 0u) {
+    const int row_b = row;
+    const bool fr_b = first_row;
+    if (bits == 0u) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          TC v = TC(0);
+      for (int i = 0; i < 8; ++i) {
+        TC v = TC(0);
 #pragma unroll
-          for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
-          p[i] = v;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if ((bits >> i) & 1u) {
-            row = rr[i];
-            load_w(row);
-          }
-          TC v = TC(0);
-#pragma unroll
-          for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
-          p[i] = v;
-        }
+        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
+        p[i] = v;
       }
-      const TC dot = reduce8(p);
-      const TC r = valid ? dot - a : TC(0);
-      if (valid) {
-        if (P.R) P.R[E0 + o + q] = (TS)r;
-        sq += (double)r * (double)r;
-      }
-      __syncwarp();
-      s_r[q] = r;
-      __syncwarp();
-      TC r8[8];
-      ld4<TC>(s_r, *reinterpret_cast<TC(*)[4]>(&r8[0]));
-      ld4<TC>(s_r + 4, *reinterpret_cast<TC(*)[4]>(&r8[4]));
-      if (bits == 0u) {
+    } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
-      } else {
-        int rw = row_b;
-        bool fr = fr_b;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if ((bits >> i) & 1u) {
-            flush(rw, fr, false);
-            fr = false;
-            rw = rr[i];
-#pragma unroll
-            for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
-          }
-#pragma unroll
-          for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+      for (int i = 0; i < 8; ++i) {
+        if ((bits >> i) & 1u) {
+          row = rr[i];
+          load_w(row);
         }
-        first_row = fr;
+        TC v = TC(0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
+        p[i] = v;
       }
+    }
+    const TC dot = reduce8(p);
+    const TC r = valid ? dot - a : TC(0);
+    if (valid) {
+      if (P.R) P.R[E0 + o + q] = (TS)r;
+      sq += (double)r * (double)r;
+    }
+    __syncwarp();
+    s_r[q] = r;
+    __syncwarp();
+    TC r8[8];
+    ld4<TC>(s_r, *reinterpret_cast<TC(*)[4]>(&r8[0]));
+    ld4<TC>(s_r + 4, *reinterpret_cast<TC(*)[4]>(&r8[4]));
+    if (bits == 0u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+    } else {
+      int rw = row_b;
+      bool fr = fr_b;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if ((bits >> i) & 1u) {
+          flush(rw, fr, false);
+          fr = false;
+          rw = rr[i];
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+      }
+      first_row = fr;
+    }
     }
   }
   cp_async_wait<0>();
   if (P.probe) {
     asm volatile("" ::"f"((float)acc.a[0]));
-    t_loop = clock64();
+    t_loop = gtimer();
   }
   if (active) {
     flush(row, first_row, true);
@@ -908,17 +915,11 @@ __device__ __forceinline__ void run_group(const Pass<TS, TC>& P, int chunk, int 
     pr[0] = t_start;
     pr[1] = t_init;
     pr[2] = t_loop;
-    pr[3] = clock64();
+    pr[3] = gtimer();
   }
-  if (P.part) {
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (q == 0 && chunk < P.nchunks) {
-      P.part[chunk] = P.want_sq ? sq : 0.0;
-      P.part[P.nchunks + chunk] = 0.0;
-      P.part[2 * P.nchunks + chunk] = 0.0;
-    }
-  }
+  for (int o = 4; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  return P.want_sq ? sq : 0.0;
 }
 
 struct SumJob {
@@ -1064,12 +1065,16 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, 
   const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;
   const int wbase = gid & ~3;
   const int gl = threadIdx.x >> 3;
+  double sq = 0.0;
   if (wbase < ntot) {  // warp-uniform
     // one inlined copy of the worker (I-cache): select the orientation's pass
     const bool second = wbase >= n0p;
     const Pass<TS, TC>& P = second ? P1 : P0;
-    run_group<TS, TC, V>(P, second ? gid - n0p : gid, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
+    sq = run_group<TS, TC, V>(P, second ? gid - n0p : gid, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
   }
+  // fold the 4 groups' sums (each group's lanes hold its sum)
+  sq += __shfl_xor_sync(0xffffffffu, sq, 8);
+  sq += __shfl_xor_sync(0xffffffffu, sq, 16);
   const int wg = (blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int nwg = (gridDim.x * kThreads) >> 5;
   empty_rows_zero(P0, k, wg, nwg);
@@ -1086,34 +1091,38 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, 
     w2 += __shfl_xor_sync(0xffffffffu, w2, o);
     h2 += __shfl_xor_sync(0xffffffffu, h2, o);
   }
-  double* wp = F.block_part;                       // [nwg][2] warp partials
-  double* bp = F.block_part + 2 * (int64_t)nwg;    // [gridDim.x][3] block partials
+  double* wp = F.block_part;                       // [nwg][3] warp partials
+  double* bp = F.block_part + 3 * (int64_t)nwg;    // [gridDim.x][3] block partials
   unsigned int* bcnt = F.counter + 1;              // [gridDim.x] per-block counters
   const int wib = threadIdx.x >> 5;
   bool last_w = false;
   if (lane == 0) {
-    wp[2 * wg] = w2;
-    wp[2 * wg + 1] = h2;
+    wp[3 * wg] = sq;
+    wp[3 * wg + 1] = w2;
+    wp[3 * wg + 2] = h2;
     asm volatile("fence.release.gpu;" ::: "memory");
     last_w = atomicAdd(&bcnt[blockIdx.x], 1u) == kThreads / 32 - 1;
   }
   last_w = __shfl_sync(0xffffffffu, last_w, 0);
   if (!last_w) return;
   // last warp of this block: fold the block's warp partials (fixed order)
-  double t1 = 0.0, t2 = 0.0;
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
   if (lane < kThreads / 32) {
     const int w = blockIdx.x * (kThreads / 32) + lane;
-    t1 = __ldcg(wp + 2 * w);
-    t2 = __ldcg(wp + 2 * w + 1);
+    t0 = __ldcg(wp + 3 * w);
+    t1 = __ldcg(wp + 3 * w + 1);
+    t2 = __ldcg(wp + 3 * w + 2);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
+    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
     t1 += __shfl_xor_sync(0xffffffffu, t1, o);
     t2 += __shfl_xor_sync(0xffffffffu, t2, o);
   }
   bool last_b = false;
   if (lane == 0) {
     bcnt[blockIdx.x] = 0u;
+    bp[3 * blockIdx.x] = t0;
     bp[3 * blockIdx.x + 1] = t1;
     bp[3 * blockIdx.x + 2] = t2;
     asm volatile("fence.release.gpu;" ::: "memory");
@@ -1124,8 +1133,8 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, 
   (void)wib;
   // last block's last warp: fold block partials and the chunk sum r^2
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-  for (int64_t i = lane; i < P0.nchunks; i += 32) u0 += __ldcg(P0.part + i);
   for (unsigned int b2 = lane; b2 < gridDim.x; b2 += 32) {
+    u0 += __ldcg(bp + 3 * b2);
     u1 += __ldcg(bp + 3 * b2 + 1);
     u2 += __ldcg(bp + 3 * b2 + 2);
   }
@@ -1322,7 +1331,7 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
     P1.out = (TS*)RtW; P1.ldout = k; P1.out_scale = out_scale; P1.want_sq = 0;
     SumJob J{};
     {
-      const size_t gb = grouped ? (size_t)grouped_grid(P0.nchunks, P1.nchunks) * (3 + 2 * (kThreads / 32)) : 0;
+      const size_t gb = grouped ? (size_t)grouped_grid(P0.nchunks, P1.nchunks) * (3 + 3 * (kThreads / 32)) : 0;
       J.block_part = c.take<double>(gb > (size_t)kEpiBlocksMax * 5 ? gb : (size_t)kEpiBlocksMax * 5);
     }
     J.counter = c.take<unsigned int>(1);
@@ -1432,7 +1441,7 @@ size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
   carve_epi(s);
   const int64_t g = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
                                  chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
-  s.take<double>((size_t)g * (3 + 2 * (kThreads / 32)));
+  s.take<double>((size_t)g * (3 + 3 * (kThreads / 32)));
   return s.off + 1024;
 }
 

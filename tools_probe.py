@@ -28,5 +28,8 @@ print(wl, "workers", len(p), "span cycles", p[:, 3].max() - t0)
 for name, a in [("init", init), ("loop", loop), ("finish", fin), ("total", tot), ("issue", p[:, 4]), ("wait", p[:, 5]), ("fetch+bits", p[:, 6]), ("lds+dot", p[:, 7]), ("reduce", p[:, 8]), ("r+acc", p[:, 9])]:
     print(f"{name:7s} mean {a.mean():9.0f} p50 {np.median(a):9.0f} p90 {np.percentile(a, 90):9.0f} max {a.max():9.0f}")
 st = p[:, 0] - t0
-print("start offsets: p50", np.median(st), "p90", np.percentile(st, 90), "max", st.max())
+print("start offsets (ns): p10", np.percentile(st, 10), "p50", np.median(st), "p90", np.percentile(st, 90), "max", st.max())
+en = p[:, 3] - t0
+print("end offsets (ns): p10", np.percentile(en, 10), "p50", np.median(en), "p90", np.percentile(en, 90), "max", en.max())
+print("units: ns (globaltimer)")
 # clocks differ per SM; use relative numbers only
