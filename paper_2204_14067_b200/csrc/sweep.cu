@@ -814,10 +814,19 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
         cols[0] = x0.x; cols[1] = x0.y; cols[2] = x0.z; cols[3] = x0.w;
         cols[4] = x1.x; cols[5] = x1.y; cols[6] = x1.z; cols[7] = x1.w;
       }
+      // lanes whose dims are all zero padding (q*V >= k) skip their gathers:
+      // the row bytes actually fetched are ceil(k/V)*16 instead of kp*4
       TS h[8][V];
+      if (q * V < k) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
+        for (int i = 0; i < 8; ++i)
+          ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < V; ++j) h[i][j] = TS(0);
+      }
       TC p[8];
     const int row_b = row;
     const bool fr_b = first_row;
@@ -1056,7 +1065,7 @@ __device__ __forceinline__ double ldv2(const void* p, int64_t i, int is_f64) {
 }
 
 template <typename TS, typename TC, int V>
-__global__ void __launch_bounds__(kThreads, (V <= 4 && sizeof(TC) == 4) ? MFG_G8_MINB : 1)
+__global__ void __launch_bounds__(kThreads, (sizeof(TC) == 4) ? MFG_G8_MINB : 1)
 k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, FusedRed F) {
   __shared__ __align__(16) int32_t s_ring[kThreads / 8][128];   // [cols|rows][2 slots][32]
   __shared__ __align__(16) TS s_vring[kThreads / 8][64];        // [2 slots][32]
