@@ -132,6 +132,173 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Packed / dual BCD (k > kSmemMaxK): the normal matrix is stored packed
+// (lower triangle, s(s+1)/2 doubles) in shared memory, s = min(d_i, k), so
+// k up to ~210 stays on chip. Rows with fewer entries than k use the
+// push-through identity
+//   (lam I_k + 2 H^T H)^{-1} 2 H^T a = 2 H^T (lam I_d + 2 H H^T)^{-1} a,
+// i.e. a d x d solve instead of k x k (H = the row's gathered factor rows).
+__device__ __forceinline__ int tri(int p, int q) { return p * (p + 1) / 2 + q; }
+
+template <typename TS>
+__global__ void __launch_bounds__(kNT)
+k_bcd_packed(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other,
+             int ldo, double lam, TS* __restrict__ out, int ldout, int smax, int* __restrict__ bad) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x;
+  const int kp = k + 1;
+  double* L = sm;                                     // [smax*(smax+1)/2]
+  double* stA = L + (size_t)smax * (smax + 1) / 2;    // [kC][kp]
+  double* stB = stA + kC * kp;                        // [kC][kp]
+  double* vec = stB + kC * kp;                        // [max(k, smax)] rhs / solution
+  double* aux = vec + (k > smax ? k : smax);          // [max(k, smax)]
+  for (int i = blockIdx.x; i < lay.nrows; i += gridDim.x) {
+    const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
+    const int d = e1 - e0;
+    if (d == 0) {
+      for (int x = tid; x < k; x += kNT) out[(int64_t)i * ldout + x] = TS(0);
+      continue;
+    }
+    const bool dual = d < k;
+    const int sdim = dual ? d : k;
+    const int npk = sdim * (sdim + 1) / 2;
+    for (int x = tid; x < npk; x += kNT) L[x] = 0.0;
+    for (int x = tid; x < sdim; x += kNT) vec[x] = 0.0;
+    __syncthreads();
+    auto stage = [&](double* st, int c0, int cn) {
+      for (int x = tid; x < kC * k; x += kNT) {
+        const int c = x / k, dd = x - c * k;
+        st[c * kp + dd] = c < cn ? (double)other[(int64_t)lay.idx[e0 + c0 + c] * ldo + dd] : 0.0;
+      }
+    };
+    if (!dual) {
+      // primal: L += sum_c h_c h_c^T (lower), vec += sum_c a_c h_c
+      for (int c0 = 0; c0 < d; c0 += kC) {
+        const int cn = min(kC, d - c0);
+        stage(stA, c0, cn);
+        if (tid < kC) aux[tid] = tid < cn ? (double)vals[e0 + c0 + tid] : 0.0;
+        __syncthreads();
+        for (int x = tid; x < npk; x += kNT) {
+          const int p = (int)((sqrtf(8.f * x + 1.f) - 1.f) * 0.5f);
+          int pp = p;
+          if (tri(pp + 1, 0) <= x) ++pp;
+          if (tri(pp, 0) > x) --pp;
+          const int q = x - tri(pp, 0);
+          double acc = 0.0;
+          for (int c = 0; c < cn; ++c) acc = fma(stA[c * kp + pp], stA[c * kp + q], acc);
+          L[x] += acc;
+        }
+        for (int dd = tid; dd < k; dd += kNT) {
+          double acc = 0.0;
+          for (int c = 0; c < cn; ++c) acc = fma(aux[c], stA[c * kp + dd], acc);
+          vec[dd] += acc;
+        }
+        __syncthreads();
+      }
+    } else {
+      // dual: L[p][q] = h_p . h_q over the row's d entries (block pairs)
+      for (int q0 = 0; q0 < d; q0 += kC) {
+        const int qn = min(kC, d - q0);
+        stage(stB, q0, qn);
+        for (int p0 = q0; p0 < d; p0 += kC) {
+          const int pn = min(kC, d - p0);
+          stage(stA, p0, pn);
+          __syncthreads();
+          for (int x = tid; x < kC * kC; x += kNT) {
+            const int pi = x / kC, qi = x - pi * kC;
+            const int p = p0 + pi, q = q0 + qi;
+            if (pi < pn && qi < qn && q <= p) {
+              double acc = 0.0;
+              for (int dd = 0; dd < k; ++dd) acc = fma(stA[pi * kp + dd], stB[qi * kp + dd], acc);
+              L[tri(p, q)] = acc;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int x = tid; x < d; x += kNT) vec[x] = (double)vals[e0 + x];
+      __syncthreads();
+    }
+    // N = lam I + 2 G (primal), or lam I_d + 2 H H^T (dual); rhs = 2b or a
+    for (int x = tid; x < npk; x += kNT) {
+      int p = (int)((sqrtf(8.f * x + 1.f) - 1.f) * 0.5f);
+      if (tri(p + 1, 0) <= x) ++p;
+      if (tri(p, 0) > x) --p;
+      const int q = x - tri(p, 0);
+      L[x] = 2.0 * L[x] + (p == q ? lam : 0.0);
+    }
+    if (!dual)
+      for (int x = tid; x < sdim; x += kNT) vec[x] *= 2.0;
+    __syncthreads();
+    // packed right-looking Cholesky N = L L^T
+    for (int j = 0; j < sdim; ++j) {
+      if (tid == 0) {
+        const double djj = L[tri(j, j)];
+        if (!(djj > 0.0)) atomicOr(bad, 1);
+        L[tri(j, j)] = sqrt(djj);
+      }
+      __syncthreads();
+      const double ljj = L[tri(j, j)];
+      for (int p = j + 1 + tid; p < sdim; p += kNT) L[tri(p, j)] /= ljj;
+      __syncthreads();
+      const int rem = sdim - j - 1;
+      const int ntr = rem * (rem + 1) / 2;
+      for (int x = tid; x < ntr; x += kNT) {
+        int a = (int)((sqrtf(8.f * x + 1.f) - 1.f) * 0.5f);
+        if (tri(a + 1, 0) <= x) ++a;
+        if (tri(a, 0) > x) --a;
+        const int b = x - tri(a, 0);
+        const int p = j + 1 + a, q = j + 1 + b;
+        L[tri(p, q)] -= L[tri(p, j)] * L[tri(q, j)];
+      }
+      __syncthreads();
+    }
+    // L y = rhs
+    for (int j = 0; j < sdim; ++j) {
+      if (tid == 0) vec[j] /= L[tri(j, j)];
+      __syncthreads();
+      const double yj = vec[j];
+      for (int p = j + 1 + tid; p < sdim; p += kNT) vec[p] -= L[tri(p, j)] * yj;
+      __syncthreads();
+    }
+    // L^T x = y
+    for (int j = sdim - 1; j >= 0; --j) {
+      if (tid == 0) vec[j] /= L[tri(j, j)];
+      __syncthreads();
+      const double xj = vec[j];
+      for (int p = tid; p < j; p += kNT) vec[p] -= L[tri(j, p)] * xj;
+      __syncthreads();
+    }
+    if (!dual) {
+      for (int x = tid; x < k; x += kNT) out[(int64_t)i * ldout + x] = (TS)vec[x];
+    } else {
+      // w = 2 H^T y
+      for (int x = tid; x < k; x += kNT) aux[x] = 0.0;
+      __syncthreads();
+      for (int c0 = 0; c0 < d; c0 += kC) {
+        const int cn = min(kC, d - c0);
+        stage(stA, c0, cn);
+        __syncthreads();
+        for (int dd = tid; dd < k; dd += kNT) {
+          double acc = 0.0;
+          for (int c = 0; c < cn; ++c) acc = fma(vec[c0 + c], stA[c * kp + dd], acc);
+          aux[dd] += acc;
+        }
+        __syncthreads();
+      }
+      for (int x = tid; x < k; x += kNT) out[(int64_t)i * ldout + x] = (TS)(2.0 * aux[x]);
+    }
+    __syncthreads();
+  }
+}
+
+size_t smem_packed(int k, int smax) {
+  const int kp = k + 1;
+  const int v = k > smax ? k : smax;
+  return ((size_t)smax * (smax + 1) / 2 + 2 * (size_t)kC * kp + 2 * (size_t)v) * sizeof(double);
+}
+
 size_t smem_bytes(int k, bool global) {
   const int kp = k + 1;
   size_t n = (size_t)kC * kp + kC + 2 * (size_t)k;
@@ -150,6 +317,19 @@ template <typename TS>
 int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, int ldo, double lam,
            void* out, int ldout, void* ws, size_t wsb, cudaStream_t stream) {
   if (lay->nrows == 0 || k == 0) return MFG_OK;
+  if (k > kSmemMaxK && smem_packed(k, k) <= 220 * 1024) {
+    Carver c(ws, wsb);
+    int* bad = c.take<int>(1);
+    MFG_REQUIRE(c.ok, "bcd workspace too small");
+    const size_t smem = smem_packed(k, k);
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd_packed<TS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MFG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+    k_bcd_packed<TS><<<grid_for_rows(lay->nrows), kNT, smem, stream>>>(
+        *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, k, bad);
+    MFG_LAUNCH_CHECK();
+    return MFG_OK;
+  }
   const bool global = k > kSmemMaxK;
   const int grid = global ? 2 * kNumSMs : grid_for_rows(lay->nrows);
   Carver c(ws, wsb);

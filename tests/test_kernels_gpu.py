@@ -233,3 +233,23 @@ def test_grouped_sweep_vs_oracle(k, dtype):
     R0, RH0 = plan.R.clone(), plan.RH.clone()
     plan.run(plan.pad(wt), plan.pad(ht))
     assert torch.equal(R0, plan.R) and torch.equal(RH0, plan.RH)
+
+
+@pytest.mark.parametrize("k", [130, 150, 200])
+def test_bcd_large_k_packed_and_dual(k):
+    """k > 128: packed shared-memory Cholesky; rows with fewer entries than k
+    take the push-through (dual) d x d solve. Rows here have ~200 entries on
+    the CSR side (primal for k <= 200) and ~15 on the CSC side (dual)."""
+    rng = np.random.default_rng(k)
+    m, n = 30, 400
+    mask = rng.random((m, n)) < 0.5
+    r, c = np.nonzero(mask)
+    v = rng.standard_normal(r.size)
+    om = orc.from_coo(m, n, r, c, v)
+    w = rng.standard_normal((m, k)) * 0.3
+    h = rng.standard_normal((n, k)) * 0.3
+    obs = D.ObservationSet.from_coo(m, n, r, c, v)
+    out = MF.bcd_epoch(obs, FactorPair(w, h), 1.7)
+    w1, h1 = orc.bcd_epoch(om, w, h, 1.7)
+    assert np.max(np.abs(_np(out.w) - w1)) < 1e-9 * max(1.0, np.abs(w1).max())
+    assert np.max(np.abs(_np(out.h) - h1)) < 1e-9 * max(1.0, np.abs(h1).max())
