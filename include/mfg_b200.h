@@ -116,12 +116,30 @@ int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src,
  * Any of R/RH/RtW may be NULL to skip that output. out_scale multiplies
  * RH and RtW (e.g. 2 for gradients). vals_csc is A in CSC order.
  * compute_f64 != 0 forces fp64 arithmetic on f32 storage.
- * ldw/ldh >= k; padding columns must be zero. With ldw == ldh == the
- * grouped width (32/64 for f32, 16/32 for f64) the single-launch grouped
- * kernel runs (row pieces finished in-kernel, last-block fp64 reductions).
+ * ldw/ldh >= k; padding columns must be zero. The single-launch grouped
+ * kernel (row pieces finished in-kernel, last-block fp64 reductions) runs
+ * when RH and RtW are both wanted and either ldw == ldh == the grouped
+ * width kp (32/64 for f32, 16/32 for f64; k <= kp), or ldw == ldh == k with
+ * k a multiple of kp/8 and k*sizeof(elem) a multiple of 16 (unpadded).
  * The workspace must be zero-filled before its first use and not shared
  * with concurrent calls; the sweep leaves its counters zeroed.           */
 size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);
+
+/* mfg_sweep from HOST factors, as a host caller of the reference's sweep
+ * (residual_on_omega + loss_quad + res.csr @ H + res.csr_t @ W,
+ * mfg/data.py:272-293, mfg/operators.py:108,117) holds them: enqueues on
+ * `stream` the H2D of W_host (m x k, row-major) and H_host (n x k) into the
+ * device factors W (ld ldw) and H (ld ldh) -- one copy each, strided when
+ * ld > k -- then the sweep, then one D2H of the packed results
+ *   out = [sums (3 doubles, padded to 32 B) | RH (m x k) | RtW (n x k)]
+ * into out_host (skipped when NULL). Host buffers should be pinned for the
+ * copies to be asynchronous. Same preconditions as mfg_sweep.            */
+int mfg_sweep_host(int dtype, int compute_f64, const mfg_layout* csr,
+                   const mfg_layout* csc, int k, const void* vals_csr,
+                   const void* vals_csc, const void* W_host, const void* H_host,
+                   void* W, int ldw, void* H, int ldh, void* R, void* out,
+                   void* out_host, double out_scale, void* workspace,
+                   size_t ws_bytes, void* stream);
 int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr,
               const mfg_layout* csc, int k, const void* vals_csr,
               const void* vals_csc, const void* W, int ldw, const void* H,

@@ -113,6 +113,37 @@ extern "C" int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr, cons
                         RH, RtW, out_scale, sums, workspace, ws_bytes, (cudaStream_t)stream);
 }
 
+extern "C" int mfg_sweep_host(int dtype, int compute_f64, const mfg_layout* csr,
+                              const mfg_layout* csc, int k, const void* vals_csr,
+                              const void* vals_csc, const void* W_host, const void* H_host,
+                              void* W, int ldw, void* H, int ldh, void* R, void* out,
+                              void* out_host, double out_scale, void* workspace, size_t ws_bytes,
+                              void* stream) {
+  MFG_REQUIRE(csr && csc, "null layout");
+  MFG_REQUIRE(W_host && H_host && W && H && out, "null buffer");
+  MFG_REQUIRE(k >= 1 && ldw >= k && ldh >= k, "need k >= 1 and ldw, ldh >= k");
+  MFG_REQUIRE(dtype == MFG_F32 || dtype == MFG_F64, "dtype must be MFG_F32 or MFG_F64");
+  const size_t es = dtype == MFG_F32 ? 4 : 8;
+  const cudaStream_t st = (cudaStream_t)stream;
+  const size_t m = (size_t)csr->nrows, n = (size_t)csc->nrows;
+  auto h2d = [&](void* dst, int ld, const void* src, size_t rows) -> cudaError_t {
+    if (rows == 0) return cudaSuccess;
+    if ((size_t)ld == (size_t)k)
+      return cudaMemcpyAsync(dst, src, rows * k * es, cudaMemcpyHostToDevice, st);
+    return cudaMemcpy2DAsync(dst, ld * es, src, k * es, k * es, rows, cudaMemcpyHostToDevice, st);
+  };
+  MFG_CUDA_CHECK(h2d(W, ldw, W_host, m));
+  MFG_CUDA_CHECK(h2d(H, ldh, H_host, n));
+  char* o = static_cast<char*>(out);
+  const int rc = mfg_sweep(dtype, compute_f64, csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R,
+                           o + 32, o + 32 + m * k * es, out_scale, reinterpret_cast<double*>(o),
+                           workspace, ws_bytes, stream);
+  if (rc != MFG_OK) return rc;
+  if (out_host)
+    MFG_CUDA_CHECK(cudaMemcpyAsync(out_host, out, 32 + (m + n) * k * es, cudaMemcpyDeviceToHost, st));
+  return MFG_OK;
+}
+
 extern "C" size_t mfg_sddmm_workspace(const mfg_layout* lay, int k) {
   return sddmm_workspace(lay, k);
 }

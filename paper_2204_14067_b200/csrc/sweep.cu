@@ -24,6 +24,12 @@
 #include <cstdlib>
 #include <vector>
 
+#ifndef MFG_FFMA2
+#define MFG_FFMA2 1
+#endif
+#ifndef MFG_FFMA2_VMAX
+#define MFG_FFMA2_VMAX 4
+#endif
 #ifndef MFG_G8_MINB
 #define MFG_G8_MINB 2
 #endif
@@ -611,6 +617,40 @@ __device__ __forceinline__ T reduce8(T (&v)[8]) {
   return v[0];
 }
 
+// Lane-partial dot w . h over the lane's V dims. fp32: packed FFMA2 on
+// (even, odd) dim pairs, then one add (V/2 + 1 issues instead of V).
+template <typename TS, typename TC, int V>
+__device__ __forceinline__ TC dotv(const TC (&w)[V], const TS (&h)[V]) {
+  if constexpr (MFG_FFMA2 && sizeof(TS) == 4 && sizeof(TC) == 4 && V % 2 == 0 && V <= MFG_FFMA2_VMAX) {
+    float2 s = __fmul2_rn(make_float2(w[0], w[1]), make_float2(h[0], h[1]));
+#pragma unroll
+    for (int j = 2; j < V; j += 2)
+      s = __ffma2_rn(make_float2(w[j], w[j + 1]), make_float2(h[j], h[j + 1]), s);
+    return s.x + s.y;
+  } else {
+    TC v = TC(0);
+#pragma unroll
+    for (int j = 0; j < V; ++j) v += w[j] * (TC)h[j];
+    return v;
+  }
+}
+
+// acc += r * h over the lane's V dims (packed FFMA2 for fp32).
+template <typename TS, typename TC, int V>
+__device__ __forceinline__ void axpyv(TC (&acc)[V], TC r, const TS (&h)[V]) {
+  if constexpr (MFG_FFMA2 && sizeof(TS) == 4 && sizeof(TC) == 4 && V % 2 == 0 && V <= MFG_FFMA2_VMAX) {
+    const float2 rr = make_float2(r, r);
+#pragma unroll
+    for (int j = 0; j < V; j += 2) {
+      const float2 t = __ffma2_rn(rr, make_float2(h[j], h[j + 1]), make_float2(acc[j], acc[j + 1]));
+      acc[j] = t.x; acc[j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[j] += r * (TC)h[j];
+  }
+}
+
 template <typename TC, int V>
 struct AccV {
   TC a[V];
@@ -719,8 +759,17 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
   const TS* __restrict__ pval = P.vals + E0 + q;
   const uint32_t* __restrict__ pbm = P.lay.bmask + (E0 >> 5);
   const TS* __restrict__ self = P.self + q * V;
-  const char* __restrict__ obase = reinterpret_cast<const char*>(P.other + q * V);
-  const uint32_t ostride = (uint32_t)kp * (uint32_t)sizeof(TS);
+  // Lanes whose dims are all zero padding (q*V >= k) either skip their
+  // gathers (32-byte slices) or, for 16-byte slices, gather lane 0's part of
+  // the same row: no extra sectors, no predication or register zeroing, and
+  // their products vanish because their self-row slice is zero padding (ABI
+  // precondition). Measured: aliasing wins at V*sizeof(TS) = 16 only.
+  constexpr bool kAlias = V * sizeof(TS) == 16;
+  const bool live = q * V < k;
+  const char* __restrict__ obase =
+      reinterpret_cast<const char*>(P.other + (kAlias && !live ? 0 : q * V));
+  const uint32_t ostride = (uint32_t)P.ldo * (uint32_t)sizeof(TS);
+  const int64_t sstride = P.lds;
   const int nvalid_all = E1 - E0;  // entries of this worker
   bool start_cross = false, end_cross = false;
   int row = 0;
@@ -733,9 +782,15 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
   bool first_row = true;
   int row_first = -1, row_last = -1;
   TC w[V];
+  // all-padding lanes hold w = 0 (with ld = k their slice is the next row)
   auto load_w = [&](int rw) {
     TS t[V];
-    ldrow<TS, TC, V>(self + (int64_t)rw * kp, t);
+    if (live) {
+      ldrow<TS, TC, V>(self + (int64_t)rw * sstride, t);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) t[v] = TS(0);
+    }
 #pragma unroll
     for (int v = 0; v < V; ++v) w[v] = (TC)t[v];
   };
@@ -814,10 +869,8 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
         cols[0] = x0.x; cols[1] = x0.y; cols[2] = x0.z; cols[3] = x0.w;
         cols[4] = x1.x; cols[5] = x1.y; cols[6] = x1.z; cols[7] = x1.w;
       }
-      // lanes whose dims are all zero padding (q*V >= k) skip their gathers:
-      // the row bytes actually fetched are ceil(k/V)*16 instead of kp*4
       TS h[8][V];
-      if (q * V < k) {
+      if (kAlias || live) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
@@ -832,12 +885,7 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
     const bool fr_b = first_row;
     if (bits == 0u) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        TC v = TC(0);
-#pragma unroll
-        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
-        p[i] = v;
-      }
+      for (int i = 0; i < 8; ++i) p[i] = dotv<TS, TC, V>(w, h[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -845,10 +893,7 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
           row = rr[i];
           load_w(row);
         }
-        TC v = TC(0);
-#pragma unroll
-        for (int j = 0; j < V; ++j) v += w[j] * (TC)h[i][j];
-        p[i] = v;
+        p[i] = dotv<TS, TC, V>(w, h[i]);
       }
     }
     const TC dot = reduce8(p);
@@ -865,9 +910,7 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
     ld4<TC>(s_r + 4, *reinterpret_cast<TC(*)[4]>(&r8[4]));
     if (bits == 0u) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+      for (int i = 0; i < 8; ++i) axpyv<TS, TC, V>(acc.a, r8[i], h[i]);
     } else {
       int rw = row_b;
       bool fr = fr_b;
@@ -880,8 +923,7 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
 #pragma unroll
           for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
         }
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc.a[j] += r8[i] * (TC)h[i][j];
+        axpyv<TS, TC, V>(acc.a, r8[i], h[i]);
       }
       first_row = fr;
     }
@@ -930,6 +972,7 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
   for (int o = 4; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
   return P.want_sq ? sq : 0.0;
 }
+
 
 struct SumJob {
   const double* part;  // [3][np]
@@ -1064,13 +1107,16 @@ __device__ __forceinline__ double ldv2(const void* p, int64_t i, int is_f64) {
   return is_f64 ? static_cast<const double*>(p)[i] : (double)static_cast<const float*>(p)[i];
 }
 
+template <typename TS, typename TC>
+__device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k,
+                                           const FusedRed& F, double sq);
+
 template <typename TS, typename TC, int V>
 __global__ void __launch_bounds__(kThreads, (sizeof(TC) == 4) ? MFG_G8_MINB : 1)
 k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, FusedRed F) {
   __shared__ __align__(16) int32_t s_ring[kThreads / 8][128];   // [cols|rows][2 slots][32]
   __shared__ __align__(16) TS s_vring[kThreads / 8][64];        // [2 slots][32]
   __shared__ __align__(16) TC s_r[kThreads / 8][8];
-  const int lane = threadIdx.x & 31;
   const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;
   const int wbase = gid & ~3;
   const int gl = threadIdx.x >> 3;
@@ -1081,6 +1127,15 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, 
     const Pass<TS, TC>& P = second ? P1 : P0;
     sq = run_group<TS, TC, V>(P, second ? gid - n0p : gid, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
   }
+  sweep_tail(P0, P1, k, F, sq);
+}
+
+// Kernel-wide tail of the fused sweep: zero the empty rows, and reduce
+// sum r^2 (per-group sums) and the dense norms |W|^2, |H|^2 in fp64.
+template <typename TS, typename TC>
+__device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k,
+                                           const FusedRed& F, double sq) {
+  const int lane = threadIdx.x & 31;
   // fold the 4 groups' sums (each group's lanes hold its sum)
   sq += __shfl_xor_sync(0xffffffffu, sq, 8);
   sq += __shfl_xor_sync(0xffffffffu, sq, 16);
@@ -1328,7 +1383,12 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
   // grouped v3 kernel: zero-padded factors of width kp, all outputs wanted
   int kpg = grouped_kp(k, (int)sizeof(TS));
   if (sizeof(TS) != sizeof(TC) && kpg > 32) kpg = 0;  // fp64 compute on fp32: V = 4 only
-  const bool grouped = kpg && ldw == kpg && ldh == kpg && acc0 && acc1 && csr->nnz > 0;
+  // factor layouts of the grouped kernel: zero-padded to kp, or unpadded
+  // (ld = k) when each lane's V-dim slice is whole and 16-byte aligned
+  const bool ld_ok = kpg && ((ldw == kpg && ldh == kpg) ||
+                             (ldw == k && ldh == k && k % (kpg / 8) == 0 &&
+                              ((size_t)k * sizeof(TS)) % 16 == 0));
+  const bool grouped = ld_ok && acc0 && acc1 && csr->nnz > 0;
   if (!setup_pass(P0, c, csr, k, acc0, true, grouped ? kpg : 0)) goto small;
   if (!setup_pass(P1, c, csc, k, acc1, false, grouped ? kpg : 0)) goto small;
   {

@@ -59,6 +59,18 @@ def grouped_width(k: int, dtype, compute_f64: bool = False) -> int:
     return 16 if k <= 16 else (32 if k <= 32 else 0)
 
 
+def grouped_ld(k: int, dtype, compute_f64: bool = False) -> int:
+    """Factor row stride the grouped sweep kernel takes without padding: k
+    itself when each lane's slice of V = kp/8 dims is whole and 16-byte
+    aligned (k % V == 0, k * elem % 16 == 0), else the padded width kp (0 =
+    grouped kernel not used)."""
+    kp = grouped_width(k, dtype, compute_f64)
+    if not kp:
+        return 0
+    elem = 4 if dtype == torch.float32 else 8
+    return k if (k % (kp // 8) == 0 and (k * elem) % 16 == 0) else kp
+
+
 class SweepPlan:
     """Pre-planned Omega sweep (mfg_sweep) with resident outputs and workspace.
 
@@ -77,34 +89,82 @@ class SweepPlan:
         self.compute_f64 = 1 if compute_f64 else 0
         self.out_scale = float(out_scale)
         self.R = torch.empty(obs.size, dtype=dt, device=dev.device) if want_r else None
-        self.RH = torch.empty((obs.m, k), dtype=dt, device=dev.device) if want_rh else None
-        self.RtW = torch.empty((obs.n, k), dtype=dt, device=dev.device) if want_rtw else None
-        self.sums = torch.zeros(3, dtype=torch.float64, device=dev.device)
+        # host-facing results in one buffer [sums (32 B) | RH | RtW], so the
+        # end-to-end path reads them back with a single D2H copy
+        es = torch.empty(0, dtype=dt).element_size()
+        nb_rh = obs.m * k * es if want_rh else 0
+        nb_rtw = obs.n * k * es if want_rtw else 0
+        self._out = torch.zeros(32 + nb_rh + nb_rtw, dtype=torch.uint8, device=dev.device)
+        self.sums = self._out[:24].view(torch.float64)
+        self.RH = self._out[32:32 + nb_rh].view(dt).view(obs.m, k) if want_rh else None
+        self.RtW = self._out[32 + nb_rh:].view(dt).view(obs.n, k) if want_rtw else None
         lib = _lib.lib()
         self.wsb = lib.mfg_sweep_workspace(dev.csr.ref, dev.csc.ref, max(self.k, 1))
         # zero-filled once: the grouped kernel keeps zero-at-rest counters here
         self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
         self.kp = grouped_width(self.k, dt, compute_f64)
+        self.ld = grouped_ld(self.k, dt, compute_f64) or self.k
+        self._host = None
 
     def pad(self, f: torch.Tensor) -> torch.Tensor:
-        """Zero-padded (rows x kp) copy of a factor: the layout of the grouped
-        sweep kernel (one 16-byte vector per lane gathers a whole row)."""
-        if not self.kp:
+        """Factor in the grouped kernel's layout: contiguous (rows x k) when
+        the kernel takes k unpadded (``ld == k``), else a zero-padded
+        (rows x kp) copy (one 16-byte vector per lane gathers a whole row)."""
+        if self.ld == self.k:
             return f.to(self.dt).contiguous()
-        out = torch.zeros((f.shape[0], self.kp), dtype=self.dt, device=self.obs.dev.device)
+        out = torch.zeros((f.shape[0], self.ld), dtype=self.dt, device=self.obs.dev.device)
         out[:, : f.shape[1]] = f
         return out
 
+    def _args(self, w: torch.Tensor, h: torch.Tensor, stream: int) -> tuple:
+        dev = self.obs.dev
+        return (_lib.dtype_code(self.dt), self.compute_f64, dev.csr.ref, dev.csc.ref, max(self.k, 1),
+                dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(), int(w.stride(0)),
+                h.data_ptr(), int(h.stride(0)),
+                _lib.ptr(self.R), _lib.ptr(self.RH), _lib.ptr(self.RtW), self.out_scale,
+                self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, stream)
+
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
         """w, h: (rows x ld) with ld = k, or the zero-padded width ``kp``."""
-        dev = self.obs.dev
-        k = max(self.k, 1)
-        _lib.check(_lib.lib().mfg_sweep(
-            _lib.dtype_code(self.dt), self.compute_f64, dev.csr.ref, dev.csc.ref, k,
-            dev.vals.data_ptr(), dev.vals_csc.data_ptr(), w.data_ptr(), int(w.stride(0)),
-            h.data_ptr(), int(h.stride(0)),
-            _lib.ptr(self.R), _lib.ptr(self.RH), _lib.ptr(self.RtW), self.out_scale,
-            self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, _lib.stream_ptr()), "sweep")
+        _lib.check(_lib.lib().mfg_sweep(*self._args(w, h, _lib.stream_ptr())), "sweep")
+
+    def run_host(self, w_host: torch.Tensor, h_host: torch.Tensor):
+        """End-to-end sweep from host factors through one ABI call
+        (mfg_sweep_host): H2D of W and H into resident device factors, the
+        sweep, and one D2H of the packed results [sums | RH | RtW]. Host
+        factors are contiguous (rows x k) CPU tensors, pinned for the copies
+        to be asynchronous. Returns pinned host views (sums, RH, RtW), valid
+        once the current stream reaches this point and until the next call."""
+        if self.RH is None or self.RtW is None:
+            raise ValueError("run_host needs a plan with want_rh and want_rtw")
+        for t, rows in ((w_host, self.obs.m), (h_host, self.obs.n)):
+            if t.device.type != "cpu" or t.dtype != self.dt or tuple(t.shape) != (rows, self.k) \
+                    or not t.is_contiguous():
+                raise ValueError(f"host factor must be a contiguous CPU ({rows} x {self.k}) {self.dt} tensor")
+        stream = torch.cuda.current_stream().cuda_stream
+        if self._host is None:
+            dev = self.obs.dev.device
+            self._wd = torch.zeros((self.obs.m, self.ld), dtype=self.dt, device=dev)
+            self._hd = torch.zeros((self.obs.n, self.ld), dtype=self.dt, device=dev)
+            self._host = torch.empty(self._out.numel(), dtype=torch.uint8).pin_memory()
+            nb_rh = self.RH.numel() * self.RH.element_size()
+            self._host_views = (self._host[:24].view(torch.float64),
+                                self._host[32:32 + nb_rh].view(self.dt).view(self.obs.m, self.k),
+                                self._host[32 + nb_rh:].view(self.dt).view(self.obs.n, self.k))
+            self._host_key = None
+        if self._host_key != stream:
+            dev = self.obs.dev
+            self._host_key = stream
+            self._host_args = (
+                _lib.dtype_code(self.dt), self.compute_f64, dev.csr.ref, dev.csc.ref, self.k,
+                dev.vals.data_ptr(), dev.vals_csc.data_ptr())
+            self._host_tail = (
+                self._wd.data_ptr(), self.ld, self._hd.data_ptr(), self.ld, _lib.ptr(self.R),
+                self._out.data_ptr(), self._host.data_ptr(), self.out_scale, self.ws.data_ptr(),
+                self.wsb, stream)
+        _lib.check(_lib.lib().mfg_sweep_host(*self._host_args, w_host.data_ptr(), h_host.data_ptr(),
+                                             *self._host_tail), "sweep_host")
+        return self._host_views
 
 
 def sweep(obs: ObservationSet, wf: FactorPair, *, want_r=False, want_rh=False, want_rtw=False,

@@ -206,8 +206,10 @@ def test_sweep_deterministic_and_identities():
 
 @pytest.mark.parametrize("k", [3, 8, 16, 20, 30, 32, 40, 64])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-def test_grouped_sweep_vs_oracle(k, dtype):
-    """The grouped (zero-padded, 8-lane group) sweep kernel."""
+@pytest.mark.parametrize("layout", ["plan", "padded"])
+def test_grouped_sweep_vs_oracle(k, dtype, layout):
+    """The grouped (8-lane group) sweep kernel, with factors in the plan's
+    layout (unpadded ld = k where the kernel takes it) and zero-padded to kp."""
     from paper_2204_14067_b200.mfsolver import SweepPlan
     m, n, r, c, v = synth.generate("c3", scale=0.03, seed=100 + k)
     m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
@@ -217,6 +219,12 @@ def test_grouped_sweep_vs_oracle(k, dtype):
     plan = SweepPlan(obs, k)
     wt = torch.as_tensor(w).to(dtype).cuda()
     ht = torch.as_tensor(h).to(dtype).cuda()
+    if layout == "padded" and plan.kp:
+        def pad(f):
+            out = torch.zeros((f.shape[0], plan.kp), dtype=dtype, device="cuda")
+            out[:, :k] = f
+            return out
+        plan.pad = pad
     plan.run(plan.pad(wt), plan.pad(ht))
     rr, rh, rtw, sq, w2, h2 = orc.sweep(om, _np(wt), _np(ht))
     tol = 1e-11 if dtype == torch.float64 else 2e-5
@@ -233,6 +241,14 @@ def test_grouped_sweep_vs_oracle(k, dtype):
     R0, RH0 = plan.R.clone(), plan.RH.clone()
     plan.run(plan.pad(wt), plan.pad(ht))
     assert torch.equal(R0, plan.R) and torch.equal(RH0, plan.RH)
+    # end-to-end entry point from host factors: same results
+    sums_h, rh_h, rtw_h = plan.run_host(torch.as_tensor(w).to(dtype).pin_memory(),
+                                        torch.as_tensor(h).to(dtype).pin_memory())
+    torch.cuda.synchronize()
+    assert torch.equal(rh_h, RH0.cpu()) and torch.equal(rtw_h, plan.RtW.cpu())
+    sh = sums_h.numpy()
+    assert sh[0] == sums[0]                              # same per-entry order
+    assert np.allclose(sh[1:], sums[1:], rtol=1e-13)     # norms: layout-dependent slices
 
 
 @pytest.mark.parametrize("k", [130, 150, 200])
