@@ -120,7 +120,7 @@ int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src,
  * kernel (row pieces finished in-kernel, last-block fp64 reductions) runs
  * when RH and RtW are both wanted and either ldw == ldh == the grouped
  * width kp (32/64 for f32, 16/32 for f64; k <= kp), or ldw == ldh == k with
- * k a multiple of kp/8 and k*sizeof(elem) a multiple of 16 (unpadded).
+ * k*sizeof(elem) a multiple of 16 (unpadded).
  * The workspace must be zero-filled before its first use and not shared
  * with concurrent calls; the sweep leaves its counters zeroed.           */
 size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);

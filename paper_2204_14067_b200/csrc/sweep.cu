@@ -574,19 +574,38 @@ k_sweep(Pass<TS, TC> P0, Pass<TS, TC> P1, int nw0, int nw_total, int k) {
 // leaves entry q's dot in lane q, then the SpMM accumulation from the same
 // registers. Row ends are rare and handled by an out-of-line flush.
 
+// Lane q's slice of a factor row is V elements in 16-byte chunks: chunk c
+// holds elements [c*8E + qE, c*8E + qE + E), E = 16 / sizeof(TS). One
+// LDG.128 instruction per chunk then covers 128 contiguous bytes of a row
+// across the 8-lane group (each sector fetched once), where a contiguous
+// 32-byte slice per lane would touch every sector with two instructions.
+template <typename TS>
+__host__ __device__ constexpr int chunk_elems() { return 16 / (int)sizeof(TS); }
+
+template <typename TS, int V>
+__device__ __forceinline__ int dim_of(int q, int v) {
+  constexpr int E = chunk_elems<TS>();
+  return (v / E) * 8 * E + q * E + (v % E);
+}
+
+// p = row base + q*E; chunks whose bit in `live` is clear are zero-filled
+// (their dims are >= k: padding or, unpadded, the next row's data).
 template <typename TS, typename TC, int V>
-__device__ __forceinline__ void ldrow(const TS* p, TS (&o)[V]) {
-  if constexpr (sizeof(TS) == 4) {
+__device__ __forceinline__ void ldrow(const TS* p, TS (&o)[V], unsigned live) {
+  constexpr int E = chunk_elems<TS>();
 #pragma unroll
-    for (int v4 = 0; v4 < V / 4; ++v4) {
-      const float4 x = reinterpret_cast<const float4*>(p)[v4];
-      o[4 * v4] = x.x; o[4 * v4 + 1] = x.y; o[4 * v4 + 2] = x.z; o[4 * v4 + 3] = x.w;
-    }
-  } else {
+  for (int c = 0; c < V / E; ++c) {
+    if ((live >> c) & 1u) {
+      if constexpr (sizeof(TS) == 4) {
+        const float4 x = *reinterpret_cast<const float4*>(p + c * 8 * E);
+        o[4 * c] = x.x; o[4 * c + 1] = x.y; o[4 * c + 2] = x.z; o[4 * c + 3] = x.w;
+      } else {
+        const double2 x = *reinterpret_cast<const double2*>(p + c * 8 * E);
+        o[2 * c] = x.x; o[2 * c + 1] = x.y;
+      }
+    } else {
 #pragma unroll
-    for (int v2 = 0; v2 < V / 2; ++v2) {
-      const double2 x = reinterpret_cast<const double2*>(p)[v2];
-      o[2 * v2] = x.x; o[2 * v2 + 1] = x.y;
+      for (int e = 0; e < E; ++e) o[c * E + e] = TS(0);
     }
   }
 }
@@ -668,7 +687,7 @@ __device__ __noinline__ void flush_group(TS* out, int ldout, double out_scale, T
     TS* o = out + (int64_t)frow * ldout;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int d = q * V + v;
+      const int d = dim_of<TS, V>(q, v);
       if (d < k) o[d] = (TS)(acc.a[v] * (TC)out_scale);
     }
   }
@@ -728,7 +747,7 @@ __device__ __noinline__ void finish_row(TS* out, int ldout, double out_scale, TC
   TS* o = out + (int64_t)frow * ldout;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
-    const int d = q * V + v;
+    const int d = dim_of<TS, V>(q, v);
     if (d < k) o[d] = (TS)(acc[v] * (TC)out_scale);
   }
   if (q == 0) row_cnt[frow] = 0;
@@ -758,16 +777,20 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
   const int32_t* __restrict__ prow = P.lay.row_of + E0 + q;
   const TS* __restrict__ pval = P.vals + E0 + q;
   const uint32_t* __restrict__ pbm = P.lay.bmask + (E0 >> 5);
-  const TS* __restrict__ self = P.self + q * V;
-  // Lanes whose dims are all zero padding (q*V >= k) either skip their
-  // gathers (32-byte slices) or, for 16-byte slices, gather lane 0's part of
-  // the same row: no extra sectors, no predication or register zeroing, and
-  // their products vanish because their self-row slice is zero padding (ABI
-  // precondition). Measured: aliasing wins at V*sizeof(TS) = 16 only.
-  constexpr bool kAlias = V * sizeof(TS) == 16;
-  const bool live = q * V < k;
+  constexpr int E = chunk_elems<TS>();
+  const TS* __restrict__ self = P.self + q * E;
+  // Chunks whose dims are all >= k are not loaded (bit c of livem clear).
+  // With one chunk per lane (16-byte slices) the all-padding lanes instead
+  // gather lane 0's chunk of the same row: no extra sectors, no predication
+  // or register zeroing, and their products vanish because their self-row
+  // slice is held at zero. Measured: aliasing wins at one chunk only.
+  constexpr bool kAlias = V == E;
+  unsigned livem = 0;
+#pragma unroll
+  for (int c = 0; c < V / E; ++c) livem |= (c * 8 * E + q * E < k ? 1u : 0u) << c;
+  const bool live = (livem & 1u) != 0;
   const char* __restrict__ obase =
-      reinterpret_cast<const char*>(P.other + (kAlias && !live ? 0 : q * V));
+      reinterpret_cast<const char*>(P.other + (kAlias && !live ? 0 : q * E));
   const uint32_t ostride = (uint32_t)P.ldo * (uint32_t)sizeof(TS);
   const int64_t sstride = P.lds;
   const int nvalid_all = E1 - E0;  // entries of this worker
@@ -785,12 +808,7 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
   // all-padding lanes hold w = 0 (with ld = k their slice is the next row)
   auto load_w = [&](int rw) {
     TS t[V];
-    if (live) {
-      ldrow<TS, TC, V>(self + (int64_t)rw * sstride, t);
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) t[v] = TS(0);
-    }
+    ldrow<TS, TC, V>(self + (int64_t)rw * sstride, t, livem);
 #pragma unroll
     for (int v = 0; v < V; ++v) w[v] = (TC)t[v];
   };
@@ -870,16 +888,10 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
         cols[4] = x1.x; cols[5] = x1.y; cols[6] = x1.z; cols[7] = x1.w;
       }
       TS h[8][V];
-      if (kAlias || live) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < V; ++j) h[i][j] = TS(0);
-      }
+      for (int i = 0; i < 8; ++i)
+        ldrow<TS, TC, V>(reinterpret_cast<const TS*>(obase + (uint64_t)(uint32_t)cols[i] * ostride), h[i],
+                         kAlias ? 1u : livem);
       TC p[8];
     const int row_b = row;
     const bool fr_b = first_row;
@@ -1384,10 +1396,9 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
   int kpg = grouped_kp(k, (int)sizeof(TS));
   if (sizeof(TS) != sizeof(TC) && kpg > 32) kpg = 0;  // fp64 compute on fp32: V = 4 only
   // factor layouts of the grouped kernel: zero-padded to kp, or unpadded
-  // (ld = k) when each lane's V-dim slice is whole and 16-byte aligned
+  // (ld = k) when rows are whole 16-byte chunks (k * sizeof(TS) % 16 == 0)
   const bool ld_ok = kpg && ((ldw == kpg && ldh == kpg) ||
-                             (ldw == k && ldh == k && k % (kpg / 8) == 0 &&
-                              ((size_t)k * sizeof(TS)) % 16 == 0));
+                             (ldw == k && ldh == k && ((size_t)k * sizeof(TS)) % 16 == 0));
   const bool grouped = ld_ok && acc0 && acc1 && csr->nnz > 0;
   if (!setup_pass(P0, c, csr, k, acc0, true, grouped ? kpg : 0)) goto small;
   if (!setup_pass(P1, c, csc, k, acc1, false, grouped ? kpg : 0)) goto small;

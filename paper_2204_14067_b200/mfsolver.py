@@ -61,14 +61,13 @@ def grouped_width(k: int, dtype, compute_f64: bool = False) -> int:
 
 def grouped_ld(k: int, dtype, compute_f64: bool = False) -> int:
     """Factor row stride the grouped sweep kernel takes without padding: k
-    itself when each lane's slice of V = kp/8 dims is whole and 16-byte
-    aligned (k % V == 0, k * elem % 16 == 0), else the padded width kp (0 =
-    grouped kernel not used)."""
+    itself when a row is whole 16-byte chunks (k * elem % 16 == 0), else the
+    padded width kp (0 = grouped kernel not used)."""
     kp = grouped_width(k, dtype, compute_f64)
     if not kp:
         return 0
     elem = 4 if dtype == torch.float32 else 8
-    return k if (k % (kp // 8) == 0 and (k * elem) % 16 == 0) else kp
+    return k if (k * elem) % 16 == 0 else kp
 
 
 class SweepPlan:
