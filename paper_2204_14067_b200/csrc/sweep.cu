@@ -887,6 +887,16 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
         cols[0] = x0.x; cols[1] = x0.y; cols[2] = x0.z; cols[3] = x0.w;
         cols[4] = x1.x; cols[5] = x1.y; cols[6] = x1.z; cols[7] = x1.w;
       }
+      // the self row of the batch's first row start is loaded before the
+      // gathers, so its latency overlaps theirs instead of serialising the
+      // dots behind it
+      int i0 = -1, row0 = 0;
+      TS w0[V];
+      if (bits) {
+        i0 = __ffs(bits) - 1;
+        row0 = rr[i0];
+        ldrow<TS, TC, V>(self + (int64_t)row0 * sstride, w0, livem);
+      }
       TS h[8][V];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -895,15 +905,39 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
       TC p[8];
     const int row_b = row;
     const bool fr_b = first_row;
+    // single-row-start specialisation: one-chunk lane slices only (with two
+    // chunks, V = 8 fp32, the extra live registers spill)
+    const bool one_start = kAlias && bits != 0u && (bits & (bits - 1u)) == 0u;
     if (bits == 0u) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) p[i] = dotv<TS, TC, V>(w, h[i]);
+    } else if (one_start) {
+      // one row start at i0: entries >= i0 use the new row (branch-free)
+      TC wn[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) wn[v] = (TC)w0[v];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        TC ws[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) ws[v] = i < i0 ? w[v] : wn[v];
+        p[i] = dotv<TS, TC, V>(ws, h[i]);
+      }
+      row = row0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) w[v] = wn[v];
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if ((bits >> i) & 1u) {
-          row = rr[i];
-          load_w(row);
+          if (i == i0) {
+            row = row0;
+#pragma unroll
+            for (int v = 0; v < V; ++v) w[v] = (TC)w0[v];
+          } else {
+            row = rr[i];
+            load_w(row);
+          }
         }
         p[i] = dotv<TS, TC, V>(w, h[i]);
       }
@@ -923,6 +957,16 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
     if (bits == 0u) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) axpyv<TS, TC, V>(acc.a, r8[i], h[i]);
+    } else if (one_start) {
+      // entries < i0 finish the current row, the rest start the new one
+#pragma unroll
+      for (int i = 0; i < 8; ++i) axpyv<TS, TC, V>(acc.a, i < i0 ? r8[i] : TC(0), h[i]);
+      flush(row_b, fr_b, false);
+      first_row = false;
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc.a[j] = TC(0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) axpyv<TS, TC, V>(acc.a, i < i0 ? TC(0) : r8[i], h[i]);
     } else {
       int rw = row_b;
       bool fr = fr_b;
@@ -1132,6 +1176,9 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, 
   const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;
   const int wbase = gid & ~3;
   const int gl = threadIdx.x >> 3;
+  // diagnostics: block entry stamps after the per-worker records
+  if (P0.probe && threadIdx.x == 0)
+    P0.probe[10 * (int64_t)(P0.nchunks + P1.nchunks) + 2 * blockIdx.x] = gtimer();
   double sq = 0.0;
   if (wbase < ntot) {  // warp-uniform
     // one inlined copy of the worker (I-cache): select the orientation's pass
@@ -1225,6 +1272,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     F.sums[1] = u1;
     F.sums[2] = u2;
     *F.counter = 0u;
+    if (P0.probe) P0.probe[10 * (int64_t)(P0.nchunks + P1.nchunks) + 2 * blockIdx.x + 1] = gtimer();
   }
 }
 
