@@ -1169,22 +1169,42 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
 
 template <typename TS, typename TC, int V>
 __global__ void __launch_bounds__(kThreads, (sizeof(TC) == 4) ? MFG_G8_MINB : 1)
-k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int n0p, int ntot, int k, int kp, FusedRed F) {
+k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int nb0, int nb1, int k, int kp, FusedRed F) {
   __shared__ __align__(16) int32_t s_ring[kThreads / 8][128];   // [cols|rows][2 slots][32]
   __shared__ __align__(16) TS s_vring[kThreads / 8][64];        // [2 slots][32]
   __shared__ __align__(16) TC s_r[kThreads / 8][8];
-  const int gid = (blockIdx.x * kThreads + threadIdx.x) >> 3;
-  const int wbase = gid & ~3;
+  __shared__ int s_ticket;
   const int gl = threadIdx.x >> 3;
   // diagnostics: block entry stamps after the per-worker records
   if (P0.probe && threadIdx.x == 0)
     P0.probe[10 * (int64_t)(P0.nchunks + P1.nchunks) + 2 * blockIdx.x] = gtimer();
+  // Pass affinity by SM: CTAs on the first nb0/(nb0+nb1) of the SMs take
+  // CSR work blocks, the others CSC, so each SM's L1 holds one gathered
+  // factor (H or W) instead of both. Blocks are handed out by tickets; a CTA
+  // whose pass is exhausted takes the other pass (the counts always fit:
+  // grid = nb0 + nb1). The last block re-zeroes the tickets.
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int pref = (int)smid * (nb0 + nb1) < kNumSMs * nb0 ? 0 : 1;
+    unsigned int* tick = F.counter + 1 + gridDim.x;
+    int t = (int)atomicAdd(&tick[pref], 1u);
+    int pass = pref;
+    if (t >= (pref ? nb1 : nb0)) {
+      pass = 1 - pref;
+      t = (int)atomicAdd(&tick[pass], 1u);
+    }
+    s_ticket = (pass << 30) | t;
+  }
+  __syncthreads();
   double sq = 0.0;
-  if (wbase < ntot) {  // warp-uniform
+  {
+    const bool second = (s_ticket >> 30) != 0;
+    const int wk = (s_ticket & ((1 << 30) - 1)) * (kThreads / 8) + gl;  // worker in its pass
     // one inlined copy of the worker (I-cache): select the orientation's pass
-    const bool second = wbase >= n0p;
     const Pass<TS, TC>& P = second ? P1 : P0;
-    sq = run_group<TS, TC, V>(P, second ? gid - n0p : gid, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
+    if (((wk & ~3) < P.nchunks))  // warp-uniform
+      sq = run_group<TS, TC, V>(P, wk, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
   }
   sweep_tail(P0, P1, k, F, sq);
 }
@@ -1272,6 +1292,8 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     F.sums[1] = u1;
     F.sums[2] = u2;
     *F.counter = 0u;
+    F.counter[1 + gridDim.x] = 0u;  // pass tickets
+    F.counter[2 + gridDim.x] = 0u;
     if (P0.probe) P0.probe[10 * (int64_t)(P0.nchunks + P1.nchunks) + 2 * blockIdx.x + 1] = gtimer();
   }
 }
@@ -1374,22 +1396,22 @@ bool setup_pass(Pass<TS, TC>& P, Carver& c, const mfg_layout* lay, int k, bool a
 }
 
 
+// CTAs of the grouped kernel: one per kThreads/8 workers of each pass.
+int grouped_blocks(int nchunks) { return (nchunks + kThreads / 8 - 1) / (kThreads / 8); }
 int grouped_grid(int n0, int n1) {
-  const int ntot = ((n0 + 3) & ~3) + ((n1 + 3) & ~3);
-  int g = (ntot + kThreads / 8 - 1) / (kThreads / 8);
+  const int g = grouped_blocks(n0) + grouped_blocks(n1);
   return g < 1 ? 1 : g;
 }
 
 template <typename TS, typename TC>
 int launch_grouped(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k, int kp,
                    const FusedRed& F, cudaStream_t stream) {
-  const int n0p = (P0.nchunks + 3) & ~3;
-  const int n1p = (P1.nchunks + 3) & ~3;
-  const int ntot = n0p + n1p;
+  const int nb0 = grouped_blocks(P0.nchunks), nb1 = grouped_blocks(P1.nchunks);
   const int grid = grouped_grid(P0.nchunks, P1.nchunks);
+  if (grid != nb0 + nb1) return MFG_ERR_ARG;  // empty passes are not launched here
   const int V = kp / 8;
   constexpr bool f32 = sizeof(TS) == 4, mixed = sizeof(TS) != sizeof(TC);
-  auto go = [&](auto kern) { kern<<<grid, kThreads, 0, stream>>>(P0, P1, n0p, ntot, k, kp, F); };
+  auto go = [&](auto kern) { kern<<<grid, kThreads, 0, stream>>>(P0, P1, nb0, nb1, k, kp, F); };
   if constexpr (f32 && !mixed) {
     if (V == 4) go(k_sweep_g8f<TS, TC, 4>);
     else go(k_sweep_g8f<TS, TC, 8>);
@@ -1437,7 +1459,7 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
   int32_t* cnt1 = c.take<int32_t>((size_t)csc->nrows + 1);
   const int ggrid = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
                                  chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
-  unsigned int* fcounter = c.take<unsigned int>((size_t)ggrid + 1);
+  unsigned int* fcounter = c.take<unsigned int>((size_t)ggrid + 3);  // fold, per-block, 2 tickets
   Pass<TS, TC> P0{}, P1{};
   const bool acc0 = RH != nullptr, acc1 = RtW != nullptr;
   // grouped v3 kernel: zero-padded factors of width kp, all outputs wanted
@@ -1563,7 +1585,7 @@ size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
   s.take<int32_t>((size_t)csc->nrows + 1);
   const int64_t gg = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
                                   chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
-  s.take<unsigned int>((size_t)gg + 1);
+  s.take<unsigned int>((size_t)gg + 3);
   carve_pass(s, csr, k, true, true);
   carve_pass(s, csc, k, true, false);
   carve_epi(s);
