@@ -1165,7 +1165,7 @@ __device__ __forceinline__ double ldv2(const void* p, int64_t i, int is_f64) {
 
 template <typename TS, typename TC>
 __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k,
-                                           const FusedRed& F, double sq);
+                                           const FusedRed& F, double sq, int lblk);
 
 template <typename TS, typename TC, int V>
 __global__ void __launch_bounds__(kThreads, (sizeof(TC) == 4) ? MFG_G8_MINB : 1)
@@ -1206,19 +1206,22 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int nb0, int nb1, int k, int kp, F
     if (((wk & ~3) < P.nchunks))  // warp-uniform
       sq = run_group<TS, TC, V>(P, wk, k, kp, s_ring[gl], s_vring[gl], s_r[gl]);
   }
-  sweep_tail(P0, P1, k, F, sq);
+  // fixed-order reductions: partial slots follow the logical work block,
+  // not the (dynamically ticketed) CTA
+  const int lblk = (s_ticket >> 30) ? nb0 + (s_ticket & ((1 << 30) - 1)) : s_ticket;
+  sweep_tail(P0, P1, k, F, sq, lblk);
 }
 
 // Kernel-wide tail of the fused sweep: zero the empty rows, and reduce
 // sum r^2 (per-group sums) and the dense norms |W|^2, |H|^2 in fp64.
 template <typename TS, typename TC>
 __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k,
-                                           const FusedRed& F, double sq) {
+                                           const FusedRed& F, double sq, int lblk) {
   const int lane = threadIdx.x & 31;
   // fold the 4 groups' sums (each group's lanes hold its sum)
   sq += __shfl_xor_sync(0xffffffffu, sq, 8);
   sq += __shfl_xor_sync(0xffffffffu, sq, 16);
-  const int wg = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int wg = (lblk * kThreads + threadIdx.x) >> 5;
   const int nwg = (gridDim.x * kThreads) >> 5;
   empty_rows_zero(P0, k, wg, nwg);
   empty_rows_zero(P1, k, wg, nwg);
@@ -1244,14 +1247,14 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     wp[3 * wg + 1] = w2;
     wp[3 * wg + 2] = h2;
     asm volatile("fence.release.gpu;" ::: "memory");
-    last_w = atomicAdd(&bcnt[blockIdx.x], 1u) == kThreads / 32 - 1;
+    last_w = atomicAdd(&bcnt[lblk], 1u) == kThreads / 32 - 1;
   }
   last_w = __shfl_sync(0xffffffffu, last_w, 0);
   if (!last_w) return;
   // last warp of this block: fold the block's warp partials (fixed order)
   double t0 = 0.0, t1 = 0.0, t2 = 0.0;
   if (lane < kThreads / 32) {
-    const int w = blockIdx.x * (kThreads / 32) + lane;
+    const int w = lblk * (kThreads / 32) + lane;
     t0 = __ldcg(wp + 3 * w);
     t1 = __ldcg(wp + 3 * w + 1);
     t2 = __ldcg(wp + 3 * w + 2);
@@ -1264,10 +1267,10 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   }
   bool last_b = false;
   if (lane == 0) {
-    bcnt[blockIdx.x] = 0u;
-    bp[3 * blockIdx.x] = t0;
-    bp[3 * blockIdx.x + 1] = t1;
-    bp[3 * blockIdx.x + 2] = t2;
+    bcnt[lblk] = 0u;
+    bp[3 * lblk] = t0;
+    bp[3 * lblk + 1] = t1;
+    bp[3 * lblk + 2] = t2;
     asm volatile("fence.release.gpu;" ::: "memory");
     last_b = atomicAdd(F.counter, 1u) == gridDim.x - 1;
   }
@@ -1294,7 +1297,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     *F.counter = 0u;
     F.counter[1 + gridDim.x] = 0u;  // pass tickets
     F.counter[2 + gridDim.x] = 0u;
-    if (P0.probe) P0.probe[10 * (int64_t)(P0.nchunks + P1.nchunks) + 2 * blockIdx.x + 1] = gtimer();
+    if (P0.probe) P0.probe[10 * (int64_t)(P0.nchunks + P1.nchunks) + 2 * lblk + 1] = gtimer();
   }
 }
 

@@ -20,6 +20,17 @@ for mod, name in [(driver, "mf_phase"), (driver, "mf_objective"), (driver, "inex
                   (eigensolver, "_ritz"), (driver, "build_warmstart"), (driver, "residual_on_omega_svd"),
                   (mfsolver, "bcd_epoch")]:
     wrap(mod, name)
+CQ = collections.Counter()
+_orig_cq = kernels._scholqr3
+def _cq(b):
+    t = time.perf_counter()
+    out = _orig_cq(b)
+    torch.cuda.synchronize()
+    key = ("ok" if out is not None else "fail", (b.shape[1] // 64) * 64)
+    CQ[key] += 1
+    T["cholqr2_" + key[0]] += time.perf_counter() - t
+    return out
+kernels._scholqr3 = _cq
 cfg = P.SolverConfig(lam=synth.CONFIGS[wl].lam, k0=synth.CONFIGS[wl].k0, max_outer_iters=iters, seed=0)
 t0 = time.perf_counter()
 x, _, trace = P.solve_mf_global(obs, None, cfg)
@@ -27,3 +38,4 @@ el = time.perf_counter() - t0
 print(wl, "iters", len(trace) - 1, "time", round(el, 2), "s; rank", x.rank, "F", trace.final().obj)
 for rec in trace.records: print("  it", rec.iter, "t=%.2f" % rec.time_s, "obj %.8g" % rec.obj, "rank", rec.rank, "k_t", rec.k_t, "sweeps", rec.eig_sweeps, "bt", rec.backtracks)
 for k_, t_ in T.most_common(): print(f"{k_:24s} {t_:8.2f}s  n={N[k_]}")
+for k_, c_ in sorted(CQ.items(), key=lambda kv: (kv[0][1], kv[0][0])): print("cholqr2", k_, c_)
