@@ -128,6 +128,9 @@ class ShardedMF:
       ops.sweep(handle, self_rows, other_full) -> (acc_rows, sumsq)
           acc_rows[i] = sum_j r_ij other_j with r_ij = self_i . other_j - a_ij
       ops.half_sweep(handle, other_full, lam) -> new self rows
+      ops.residual(handle, self_rows, other_full) -> r values (handle order)
+      ops.spmm(handle, vals, block_full) -> rows sum_j vals_ij block_j
+    (the last two serve the sharded lifting step, ``sharded_lift``).
     """
 
     def __init__(self, shard: Shard, ops, comm: Comm, device):
@@ -195,3 +198,19 @@ class DeviceOps:
         from .mfsolver import _half_sweep
 
         return _half_sweep(obs, False, other_full, lam)
+
+    def residual(self, obs, self_rows, other_full):
+        """r on the shard (fp64, the handle's CSR order): self_i . other_j - a_ij."""
+        from .data import sddmm
+
+        vals, _ = sddmm(obs, self_rows.to(obs.dtype).double(), other_full.to(obs.dtype).double(),
+                        dtype=torch.float64)
+        return vals
+
+    def spmm(self, obs, vals, block_full):
+        """sum_j vals_ij block_j for the shard's rows (fp64, libmfg_b200 mfg_spmm)."""
+        from .data import SparseResidual
+        from .operators import spmm
+
+        out = torch.zeros((obs.m, block_full.shape[1]), dtype=torch.float64, device=block_full.device)
+        return spmm(SparseResidual(obs.m, obs.n, obs, vals), block_full.double(), False, 1.0, 0.0, out)

@@ -31,6 +31,12 @@ class OracleOps:
         o = other_full.numpy()
         return torch.as_tensor(orc.half_sweep(om.a_csr, om.pattern_csr, o, lam))
 
+    def residual(self, om, self_rows, other_full):
+        return torch.as_tensor(orc.residual(om, self_rows.numpy(), other_full.numpy()))
+
+    def spmm(self, om, vals, block_full):
+        return torch.as_tensor(orc.spmm_csr(om, vals.numpy(), block_full.numpy()))
+
 
 def _instance():
     m, n, r, c, v = synth.generate("c2", scale=0.05, seed=11)
@@ -140,3 +146,108 @@ def test_two_shard_decomposition_on_gpu():
     assert sum(sqs) == pytest.approx(float(sums[0]), rel=1e-12)
     w1 = MF.bcd_epoch(obs, FactorPair(W, H), 3.0).w
     assert torch.equal(torch.cat(w1_parts), w1)
+
+
+# ---------------------------------------------------------------------------
+# sharded lifting step (sharded_lift): partial SVD of Z = W H^T - alpha G
+
+
+LIFT_ALPHA = 0.35
+LIFT_K = 5
+
+
+def _lift_run(world_rank, world, ops, device):
+    """Shared body: sharded operator, LM-Krylov top-k, projection, SVD and
+    soft-threshold; returns gathered results (identical on every rank)."""
+    from paper_2204_14067_b200 import sharded_lift as SL
+    from paper_2204_14067_b200.eigensolver import EigConfig
+
+    m, n, r, c, v, w, h = _instance()
+    shard = sharding.make_shard(m, n, r, c, v, world_rank, world)
+    comm = SL.ShardComm()
+    mf = sharding.ShardedMF(shard, ops, comm, device)
+    W, H = torch.as_tensor(w).to(device), torch.as_tensor(h).to(device)
+    r0_, r1_ = shard.row_block
+    c0_, c1_ = shard.col_block
+    g_row = 2.0 * ops.residual(mf.hr, W[r0_:r1_], H)
+    g_col = 2.0 * ops.residual(mf.hc, H[c0_:c1_], W)
+    op = SL.ShardedOperator(mf, comm, W, H, g_row, g_col, LIFT_ALPHA)
+    rng = np.random.default_rng(7)
+    r0 = torch.as_tensor(rng.standard_normal((m, LIFT_K))).to(device)
+    cfg = EigConfig(memory=3, max_iters=40, residual_tol=1e-9)
+    u_loc, sigma, v_loc, eig, largest = SL.partial_svd_step(op, r0[r0_:r1_], cfg, beta=0.05)
+    u = comm.allgather_blocks(u_loc, shard.row_blocks)
+    vv = comm.allgather_blocks(v_loc, shard.col_blocks)
+    basis = comm.allgather_blocks(eig.basis, shard.row_blocks)
+    return dict(eigvals=eig.eigvals, iters=eig.iters_used, res=eig.residuals, sigma=sigma,
+                x=(u.double() * torch.as_tensor(sigma).to(device)) @ vv.double().T,
+                proj=basis @ basis.T)
+
+
+def _lift_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = _lift_run(rank, world, OracleOps(), torch.device("cpu"))
+        np.savez(os.path.join(out_dir, f"l{rank}.npz"), eigvals=out["eigvals"], iters=out["iters"],
+                 sigma=out["sigma"], x=out["x"].numpy(), proj=out["proj"].numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _dense_z():
+    m, n, r, c, v, w, h = _instance()
+    om = orc.from_coo(m, n, r, c, v)
+    g = 2.0 * orc.residual(om, w, h)
+    gd = orc.csr_of(om, g).toarray()
+    return w @ h.T - LIFT_ALPHA * gd
+
+
+def test_sharded_lifting_two_ranks_gloo():
+    """2 ranks over gloo (oracle SpMMs) vs 1 rank vs a dense eigendecomposition:
+    same iteration count and identified rank; Ritz values, soft-thresholded
+    spectrum and the new iterate X agree to rounding."""
+    one = _lift_run(0, 1, OracleOps(), torch.device("cpu"))
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_lift_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [np.load(os.path.join(d, f"l{p}.npz")) for p in range(2)]
+    for x in res:
+        assert int(x["iters"]) == one["iters"]
+        assert x["sigma"].size == one["sigma"].size
+        np.testing.assert_allclose(x["eigvals"], one["eigvals"], rtol=1e-11)
+        np.testing.assert_allclose(x["sigma"], one["sigma"], rtol=1e-11)
+        np.testing.assert_allclose(x["x"], one["x"].numpy(), rtol=0, atol=1e-10 * np.abs(x["x"]).max())
+    # every rank holds identical bits
+    assert np.array_equal(res[0]["sigma"], res[1]["sigma"])
+    assert np.array_equal(res[0]["x"], res[1]["x"])
+    # against a dense eigendecomposition of Z Z^T
+    z = _dense_z()
+    ev = np.sort(np.linalg.eigvalsh(z @ z.T))[::-1][:LIFT_K]
+    np.testing.assert_allclose(one["eigvals"], ev, rtol=1e-8)
+    s_hat = np.sqrt(ev)
+    kept = s_hat[s_hat > 0.05] - 0.05
+    np.testing.assert_allclose(one["sigma"], kept, rtol=1e-8)
+
+
+@pytest.mark.gpu
+def test_sharded_lifting_one_rank_on_gpu_matches_product():
+    """The sharded lifting code with DeviceOps (libmfg_b200 SpMMs) at world 1
+    against the product eigensolver on the same operator."""
+    from paper_2204_14067_b200 import eigensolver as E
+    from paper_2204_14067_b200.data import ObservationSet, residual_on_omega
+    from paper_2204_14067_b200.operators import FactorPair, ShiftedOperator
+
+    got = _lift_run(0, 1, sharding.DeviceOps(torch.float64), torch.device("cuda"))
+    m, n, r, c, v, w, h = _instance()
+    obs = ObservationSet.from_coo(m, n, r, c, v)
+    wf = FactorPair(torch.as_tensor(w).cuda(), torch.as_tensor(h).cuda())
+    grad = residual_on_omega(obs, wf).scaled(2.0)
+    op = ShiftedOperator(wf, grad, LIFT_ALPHA)
+    r0 = torch.as_tensor(np.random.default_rng(7).standard_normal((m, LIFT_K))).cuda()
+    ref = E.lmkrylov_topk(op, r0, E.EigConfig(memory=3, max_iters=40, residual_tol=1e-9))
+    assert got["iters"] == ref.iters_used
+    np.testing.assert_allclose(got["eigvals"], ref.eigvals, rtol=1e-11)
+    z = _dense_z()
+    ev = np.sort(np.linalg.eigvalsh(z @ z.T))[::-1][:LIFT_K]
+    np.testing.assert_allclose(got["eigvals"], ev, rtol=1e-8)
