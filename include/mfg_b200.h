@@ -194,6 +194,21 @@ int mfg_dot(int dtype, int64_t count, const void* x, const void* y,
  * launches (0 disables), then collect the summed milliseconds.            */
 int mfg_profile_enable(int max_records);
 int mfg_profile_collect(double* total_ms, int* count);
+/* ---- text ingest (host) -------------------------------------------------
+ * Multi-threaded parser of the whitespace "user item rating [timestamp]"
+ * format (replaces mfg/data.py:164-200 _parse_stream on files/bytes).
+ * mfg_count_lines gives an upper bound on the records. mfg_parse_ratings
+ * fills users/items/ratings (cap entries) in file order and sets *count;
+ * it returns MFG_ERR_ARG with *first_odd_line (1-based) at the first line
+ * whose parse is not a plain ASCII "id id decimal [field]" with positive
+ * ids -- the caller then re-parses with the reference's rules, which accept
+ * the line or raise the reference's exact ParseError. nthreads <= 0 uses
+ * all hardware threads.                                                     */
+int64_t mfg_count_lines(const char* buf, size_t len);
+int mfg_parse_ratings(const char* buf, size_t len, int nthreads, int64_t* users,
+                      int64_t* items, double* ratings, size_t cap, size_t* count,
+                      int64_t* first_odd_line);
+
 /* per-worker clock64 stamps of the grouped sweep (start, init, loop, end),
  * [workers][4] int64 on the device; NULL disables.                        */
 int mfg_set_probe(void* dev_buffer);

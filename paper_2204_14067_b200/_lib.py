@@ -54,6 +54,8 @@ _SIGS = {
     "mfg_last_error": (ctypes.c_char_p, []),
     "mfg_version": (_INT, []),
     "mfg_launch_count": (_I64, []),
+    "mfg_count_lines": (_I64, [_P, _SZ]),
+    "mfg_parse_ratings": (_INT, [_P, _SZ, _INT, _P, _P, _P, _SZ, _P, _P]),
     "mfg_omega_build_workspace": (_SZ, [_I64, _I32, _I32]),
     "mfg_omega_build": (_INT, [_I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                ctypes.POINTER(_I64), ctypes.POINTER(_I32), _P, _SZ, _P]),

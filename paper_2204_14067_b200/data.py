@@ -498,12 +498,143 @@ def _parse_stream(stream, what: str):
             np.asarray(ratings, dtype=np.float64))
 
 
-def _open_lines(source):
-    if isinstance(source, (str, os.PathLike)):
-        return open(source, "rb")
-    if isinstance(source, bytes):
-        return io.BytesIO(source)
-    return source
+def _parse_native(buf: bytes):
+    """libmfg_b200 mfg_parse_ratings on an in-memory file (multi-threaded);
+    None when a line needs the reference's rules (the caller re-parses)."""
+    import ctypes
+
+    from . import _lib
+
+    lib = _lib.lib()
+    cap = int(lib.mfg_count_lines(buf, len(buf)))
+    users = np.empty(cap, dtype=np.int64)
+    items = np.empty(cap, dtype=np.int64)
+    ratings = np.empty(cap, dtype=np.float64)
+    count = ctypes.c_size_t(0)
+    odd = ctypes.c_int64(0)
+    st = lib.mfg_parse_ratings(buf, len(buf), 0, users.ctypes.data, items.ctypes.data,
+                               ratings.ctypes.data, cap, ctypes.byref(count), ctypes.byref(odd))
+    if st != _lib.MFG_OK:
+        return None
+    c = int(count.value)
+    return users[:c], items[:c], ratings[:c]
+
+
+def _parse_source(source, what: str):
+    """Parse a path, bytes or an iterable of lines. Files and bytes go through
+    the native parser; a line it does not take (or an iterable source) is
+    parsed with the reference's rules (mfg/data.py:164-200), so accepted
+    values and raised errors are the reference's."""
+    if isinstance(source, (str, os.PathLike, bytes)):
+        if isinstance(source, bytes):
+            buf = source
+        else:
+            with open(source, "rb") as fh:
+                buf = fh.read()
+        out = _parse_native(buf)
+        if out is not None:
+            if out[0].size == 0:
+                raise EmptyDatasetError(f"no ratings found in {what}")
+            return out
+        return _parse_stream(io.BytesIO(buf), what)
+    return _parse_stream(source, what)
+
+
+INSTANCE_MAGIC = b"MFGOMEG1"
+_INSTANCE_FIELDS = 8   # int64 header words after the magic
+
+
+def write_instance(path, m: int, n: int, rows, cols, vals, transposed: bool = False,
+                   row_ids=None, col_ids=None, split: "EvalSplit | None" = None) -> None:
+    """Binary Omega instance, the at-scale stand-in
+    for re-parsing text with load_ratings (mfg/data.py:203-250): the magic,
+    8 little-endian int64 words (m, n, nnz, transposed, value bytes, #row ids,
+    #col ids, #test entries), then 8-byte aligned arrays: rows, cols (int32),
+    values (f32 or f64), row ids, col ids (int64), test rows, cols (int32) and
+    values (f64). Entries are stored as given (canonical order when written
+    from an ObservationSet)."""
+    rows = np.ascontiguousarray(rows, dtype=np.int32)
+    cols = np.ascontiguousarray(cols, dtype=np.int32)
+    vals = np.ascontiguousarray(vals)
+    if vals.dtype not in (np.float32, np.float64):
+        vals = vals.astype(np.float64)
+    if not (rows.size == cols.size == vals.size):
+        raise ValueError("rows, cols and vals must have the same length")
+    rid = np.zeros(0, np.int64) if row_ids is None else np.ascontiguousarray(row_ids, dtype=np.int64)
+    cid = np.zeros(0, np.int64) if col_ids is None else np.ascontiguousarray(col_ids, dtype=np.int64)
+    if split is not None:
+        tr, tc = np.asarray(split.rows, np.int32), np.asarray(split.cols, np.int32)
+        tv = np.asarray(split.vals, np.float64)
+    else:
+        tr = tc = np.zeros(0, np.int32)
+        tv = np.zeros(0, np.float64)
+    head = np.array([m, n, rows.size, int(bool(transposed)), vals.itemsize, rid.size, cid.size, tr.size],
+                    dtype="<i8")
+    with open(path, "wb") as fh:
+        fh.write(INSTANCE_MAGIC)
+        fh.write(head.tobytes())
+        for a in (rows, cols, vals, rid, cid, tr, tc, tv):
+            b = a.astype(a.dtype.newbyteorder("<"), copy=False).tobytes()
+            fh.write(b)
+            if len(b) % 8:
+                fh.write(b"\0" * (8 - len(b) % 8))
+
+
+def read_instance(path) -> dict:
+    """Host arrays of a binary Omega instance (one read per array)."""
+    with open(path, "rb") as fh:
+        if fh.read(len(INSTANCE_MAGIC)) != INSTANCE_MAGIC:
+            raise DatasetError(f"{path}: not an Omega instance file")
+        head = np.frombuffer(fh.read(8 * _INSTANCE_FIELDS), dtype="<i8")
+        if head.size != _INSTANCE_FIELDS:
+            raise DatasetError(f"{path}: truncated header")
+        m, n, nnz, tr, vb, nr, nc, nt = (int(x) for x in head)
+        if vb not in (4, 8) or min(m, n, nnz, nr, nc, nt) < 0:
+            raise DatasetError(f"{path}: corrupt header")
+        out = {"m": m, "n": n, "transposed": bool(tr)}
+
+        def arr(name, dt, count):
+            a = np.fromfile(fh, dtype=dt, count=count)
+            if a.size != count:
+                raise DatasetError(f"{path}: truncated {name}")
+            pad = (-count * np.dtype(dt).itemsize) % 8
+            if pad:
+                fh.read(pad)
+            out[name] = a
+
+        arr("rows", "<i4", nnz)
+        arr("cols", "<i4", nnz)
+        arr("vals", "<f4" if vb == 4 else "<f8", nnz)
+        arr("row_ids", "<i8", nr)
+        arr("col_ids", "<i8", nc)
+        arr("test_rows", "<i4", nt)
+        arr("test_cols", "<i4", nt)
+        arr("test_vals", "<f8", nt)
+    return out
+
+
+def save_instance(path, obs: "ObservationSet", split: "EvalSplit | None" = None) -> None:
+    """Write an ObservationSet (and optional test split) as a binary instance."""
+    vals = obs.vals
+    write_instance(path, obs.m, obs.n, obs.rows, obs.cols,
+                   vals.astype(np.float32) if obs.dtype == torch.float32 else vals,
+                   obs.transposed, obs.row_ids, obs.col_ids, split)
+
+
+def load_instance(path, dtype=None):
+    """(ObservationSet, EvalSplit | None) from a binary instance; the device
+    build validates the entries exactly as from_coo does."""
+    a = read_instance(path)
+    if dtype is None:
+        dtype = torch.float32 if a["vals"].dtype == np.float32 else torch.float64
+    obs = ObservationSet.from_coo(a["m"], a["n"], a["rows"], a["cols"], a["vals"], a["transposed"],
+                                  a["row_ids"] if a["row_ids"].size else None,
+                                  a["col_ids"] if a["col_ids"].size else None, dtype=dtype)
+    split = None
+    if a["test_rows"].size:
+        split = EvalSplit(a["m"], a["n"], a["test_rows"].astype(np.int64), a["test_cols"].astype(np.int64),
+                          a["test_vals"], a["transposed"])
+    return obs, split
 
 
 def load_ratings(source, test_source=None, fmt: str = "movielens-tsv", dtype=torch.float64):
@@ -511,12 +642,10 @@ def load_ratings(source, test_source=None, fmt: str = "movielens-tsv", dtype=tor
     id compaction over train+test, transpose to m <= n."""
     if fmt != "movielens-tsv":
         raise DatasetError(f"unsupported format: {fmt}")
-    with _open_lines(source) as fh:
-        users, items, ratings = _parse_stream(fh, "training data")
+    users, items, ratings = _parse_source(source, "training data")
     test_raw = None
     if test_source is not None:
-        with _open_lines(test_source) as fh:
-            test_raw = _parse_stream(fh, "test data")
+        test_raw = _parse_source(test_source, "test data")
     all_users = users if test_raw is None else np.concatenate([users, test_raw[0]])
     all_items = items if test_raw is None else np.concatenate([items, test_raw[1]])
     uniq_users, uniq_items = np.unique(all_users), np.unique(all_items)
