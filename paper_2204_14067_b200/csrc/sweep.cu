@@ -1225,9 +1225,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   const int nwg = (gridDim.x * kThreads) >> 5;
   empty_rows_zero(P0, k, wg, nwg);
   empty_rows_zero(P1, k, wg, nwg);
-  // per-warp fp64 partials of the dense norms (fixed slices), then a
-  // barrier-free two-level last-arriver reduction: the last warp of each
-  // block folds its block's warp partials, the last block folds the blocks.
+  // per-warp fp64 partials of the dense norms (fixed slices)
   const int64_t gl0 = (int64_t)wg * 32 + lane, gstride = (int64_t)nwg * 32;
   double w2 = 0.0, h2 = 0.0;
   for (int64_t i = gl0; i < F.wcount; i += gstride) { const double x = ldv2(F.W, i, F.is_f64); w2 += x * x; }
@@ -1237,49 +1235,37 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     w2 += __shfl_xor_sync(0xffffffffu, w2, o);
     h2 += __shfl_xor_sync(0xffffffffu, h2, o);
   }
-  double* wp = F.block_part;                       // [nwg][3] warp partials
-  double* bp = F.block_part + 3 * (int64_t)nwg;    // [gridDim.x][3] block partials
-  unsigned int* bcnt = F.counter + 1;              // [gridDim.x] per-block counters
+  // One-level last-arriver fold: the CTA sums its warps' partials in shared
+  // memory (fixed order) and publishes them; the last CTA to arrive sums the
+  // block partials with all its threads (fixed assignment + fixed tree).
+  __shared__ double s_part[kThreads / 32][3];
+  __shared__ int s_last;
+  double* bp = F.block_part;   // [gridDim.x][3] block partials
   const int wib = threadIdx.x >> 5;
-  bool last_w = false;
   if (lane == 0) {
-    wp[3 * wg] = sq;
-    wp[3 * wg + 1] = w2;
-    wp[3 * wg + 2] = h2;
-    asm volatile("fence.release.gpu;" ::: "memory");
-    last_w = atomicAdd(&bcnt[lblk], 1u) == kThreads / 32 - 1;
+    s_part[wib][0] = sq;
+    s_part[wib][1] = w2;
+    s_part[wib][2] = h2;
   }
-  last_w = __shfl_sync(0xffffffffu, last_w, 0);
-  if (!last_w) return;
-  // last warp of this block: fold the block's warp partials (fixed order)
-  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-  if (lane < kThreads / 32) {
-    const int w = lblk * (kThreads / 32) + lane;
-    t0 = __ldcg(wp + 3 * w);
-    t1 = __ldcg(wp + 3 * w + 1);
-    t2 = __ldcg(wp + 3 * w + 2);
-  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-    t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-  }
-  bool last_b = false;
-  if (lane == 0) {
-    bcnt[lblk] = 0u;
-    bp[3 * lblk] = t0;
-    bp[3 * lblk + 1] = t1;
-    bp[3 * lblk + 2] = t2;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      b0 += s_part[w][0];
+      b1 += s_part[w][1];
+      b2 += s_part[w][2];
+    }
+    bp[3 * lblk] = b0;
+    bp[3 * lblk + 1] = b1;
+    bp[3 * lblk + 2] = b2;
     asm volatile("fence.release.gpu;" ::: "memory");
-    last_b = atomicAdd(F.counter, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(F.counter, 1u) == gridDim.x - 1;
   }
-  last_b = __shfl_sync(0xffffffffu, last_b, 0);
-  if (!last_b) return;
-  (void)wib;
-  // last block's last warp: fold block partials and the chunk sum r^2
+  __syncthreads();
+  if (!s_last) return;
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-  for (unsigned int b2 = lane; b2 < gridDim.x; b2 += 32) {
+  for (unsigned int b2 = threadIdx.x; b2 < gridDim.x; b2 += kThreads) {
     u0 += __ldcg(bp + 3 * b2);
     u1 += __ldcg(bp + 3 * b2 + 1);
     u2 += __ldcg(bp + 3 * b2 + 2);
@@ -1290,10 +1276,24 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     u1 += __shfl_xor_sync(0xffffffffu, u1, o);
     u2 += __shfl_xor_sync(0xffffffffu, u2, o);
   }
+  __syncthreads();  // s_part reuse
   if (lane == 0) {
-    F.sums[0] = u0;
-    F.sums[1] = u1;
-    F.sums[2] = u2;
+    s_part[wib][0] = u0;
+    s_part[wib][1] = u1;
+    s_part[wib][2] = u2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      v0 += s_part[w][0];
+      v1 += s_part[w][1];
+      v2 += s_part[w][2];
+    }
+    F.sums[0] = v0;
+    F.sums[1] = v1;
+    F.sums[2] = v2;
     *F.counter = 0u;
     F.counter[1 + gridDim.x] = 0u;  // pass tickets
     F.counter[2 + gridDim.x] = 0u;
