@@ -15,22 +15,22 @@ def wrap(mod, name):
         torch.cuda.synchronize(); T[name] += time.perf_counter() - t; N[name] += 1
         return out
     setattr(mod, name, g)
-for mod, name in [(driver, "mf_phase"), (driver, "mf_objective"), (driver, "inexact_prox_step"), (proxlift, "solve_topk"),
+for mod, name in [(operators, "spmm"), (driver, "mf_phase"), (driver, "mf_objective"), (driver, "inexact_prox_step"), (proxlift, "solve_topk"),
                   (proxlift, "certify_epsilon"), (proxlift, "exact_svd_short_fat"), (eigensolver, "orthonormalize"),
                   (eigensolver, "_ritz"), (driver, "build_warmstart"), (driver, "residual_on_omega_svd"),
                   (mfsolver, "bcd_epoch")]:
     wrap(mod, name)
 CQ = collections.Counter()
-_orig_cq = kernels._scholqr3
-def _cq(b):
+_orig_cq = kernels._cholqr2
+def _cq(b, scale, tol):
     t = time.perf_counter()
-    out = _orig_cq(b)
+    out = _orig_cq(b, scale, tol)
     torch.cuda.synchronize()
     key = ("ok" if out is not None else "fail", (b.shape[1] // 64) * 64)
     CQ[key] += 1
     T["cholqr2_" + key[0]] += time.perf_counter() - t
     return out
-kernels._scholqr3 = _cq
+kernels._cholqr2 = _cq
 cfg = P.SolverConfig(lam=synth.CONFIGS[wl].lam, k0=synth.CONFIGS[wl].k0, max_outer_iters=iters, seed=0)
 t0 = time.perf_counter()
 x, _, trace = P.solve_mf_global(obs, None, cfg)
