@@ -31,6 +31,15 @@ def _cq(b, scale, tol):
     T["cholqr2_" + key[0]] += time.perf_counter() - t
     return out
 kernels._cholqr2 = _cq
+_orig_qr = torch.linalg.qr
+QRN = collections.Counter()
+def _qr(a, mode="reduced"):
+    QRN[(a.shape[1] // 128) * 128] += 1
+    torch.cuda.synchronize(); t = time.perf_counter()
+    out = _orig_qr(a, mode=mode)
+    torch.cuda.synchronize(); T["householder_qr"] += time.perf_counter() - t
+    return out
+kernels.torch.linalg.qr = _qr
 cfg = P.SolverConfig(lam=synth.CONFIGS[wl].lam, k0=synth.CONFIGS[wl].k0, max_outer_iters=iters, seed=0)
 t0 = time.perf_counter()
 x, _, trace = P.solve_mf_global(obs, None, cfg)
@@ -39,3 +48,4 @@ print(wl, "iters", len(trace) - 1, "time", round(el, 2), "s; rank", x.rank, "F",
 for rec in trace.records: print("  it", rec.iter, "t=%.2f" % rec.time_s, "obj %.8g" % rec.obj, "rank", rec.rank, "k_t", rec.k_t, "sweeps", rec.eig_sweeps, "bt", rec.backtracks)
 for k_, t_ in T.most_common(): print(f"{k_:24s} {t_:8.2f}s  n={N[k_]}")
 for k_, c_ in sorted(CQ.items(), key=lambda kv: (kv[0][1], kv[0][0])): print("cholqr2", k_, c_)
+print("householder qr calls by width:", sorted(QRN.items()))
