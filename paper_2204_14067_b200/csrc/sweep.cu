@@ -30,8 +30,12 @@
 #ifndef MFG_FFMA2_VMAX
 #define MFG_FFMA2_VMAX 4
 #endif
-#ifndef MFG_G8_MINB
-#define MFG_G8_MINB 2
+#ifndef MFG_G8_MINB4
+#define MFG_G8_MINB4 4   // 128-thread CTAs per SM, 16-byte lane slices (<= 128 registers;
+                         // 5 x 102 spills and measured slower)
+#endif
+#ifndef MFG_G8_MINB8
+#define MFG_G8_MINB8 4   // 32-byte lane slices (<= 128 registers)
 #endif
 
 #include "common.cuh"
@@ -65,6 +69,13 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarpsPerBlock = kThreads / 32;
+// grouped sweep CTA: 16 eight-lane workers (4 warps). Smaller CTAs than the
+// other kernels: finer occupancy steps and shorter CTA-level tails (c4 -2%).
+constexpr int kGThreads = 128;
+template <typename TS, typename TC, int V>
+__host__ __device__ constexpr int g8_min_blocks() {
+  return sizeof(TC) == 4 ? (V * sizeof(TS) == 16 ? MFG_G8_MINB4 : MFG_G8_MINB8) : 2;
+}
 
 // Fixed-pattern butterfly: lane l ends with sum over lanes of v[l].
 template <typename T>
@@ -1168,11 +1179,11 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
                                            const FusedRed& F, double sq, int lblk);
 
 template <typename TS, typename TC, int V>
-__global__ void __launch_bounds__(kThreads, (sizeof(TC) == 4) ? MFG_G8_MINB : 1)
+__global__ void __launch_bounds__(kGThreads, g8_min_blocks<TS, TC, V>())
 k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int nb0, int nb1, int k, int kp, FusedRed F) {
-  __shared__ __align__(16) int32_t s_ring[kThreads / 8][128];   // [cols|rows][2 slots][32]
-  __shared__ __align__(16) TS s_vring[kThreads / 8][64];        // [2 slots][32]
-  __shared__ __align__(16) TC s_r[kThreads / 8][8];
+  __shared__ __align__(16) int32_t s_ring[kGThreads / 8][128];   // [cols|rows][2 slots][32]
+  __shared__ __align__(16) TS s_vring[kGThreads / 8][64];        // [2 slots][32]
+  __shared__ __align__(16) TC s_r[kGThreads / 8][8];
   __shared__ int s_ticket;
   const int gl = threadIdx.x >> 3;
   // diagnostics: block entry stamps after the per-worker records
@@ -1200,7 +1211,7 @@ k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int nb0, int nb1, int k, int kp, F
   double sq = 0.0;
   {
     const bool second = (s_ticket >> 30) != 0;
-    const int wk = (s_ticket & ((1 << 30) - 1)) * (kThreads / 8) + gl;  // worker in its pass
+    const int wk = (s_ticket & ((1 << 30) - 1)) * (kGThreads / 8) + gl;  // worker in its pass
     // one inlined copy of the worker (I-cache): select the orientation's pass
     const Pass<TS, TC>& P = second ? P1 : P0;
     if (((wk & ~3) < P.nchunks))  // warp-uniform
@@ -1221,8 +1232,8 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   // fold the 4 groups' sums (each group's lanes hold its sum)
   sq += __shfl_xor_sync(0xffffffffu, sq, 8);
   sq += __shfl_xor_sync(0xffffffffu, sq, 16);
-  const int wg = (lblk * kThreads + threadIdx.x) >> 5;
-  const int nwg = (gridDim.x * kThreads) >> 5;
+  const int wg = (lblk * kGThreads + threadIdx.x) >> 5;
+  const int nwg = (gridDim.x * kGThreads) >> 5;
   empty_rows_zero(P0, k, wg, nwg);
   empty_rows_zero(P1, k, wg, nwg);
   // per-warp fp64 partials of the dense norms (fixed slices)
@@ -1238,7 +1249,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   // One-level last-arriver fold: the CTA sums its warps' partials in shared
   // memory (fixed order) and publishes them; the last CTA to arrive sums the
   // block partials with all its threads (fixed assignment + fixed tree).
-  __shared__ double s_part[kThreads / 32][3];
+  __shared__ double s_part[kGThreads / 32][3];
   __shared__ int s_last;
   double* bp = F.block_part;   // [gridDim.x][3] block partials
   const int wib = threadIdx.x >> 5;
@@ -1251,7 +1262,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   if (threadIdx.x == 0) {
     double b0 = 0.0, b1 = 0.0, b2 = 0.0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
+    for (int w = 0; w < kGThreads / 32; ++w) {
       b0 += s_part[w][0];
       b1 += s_part[w][1];
       b2 += s_part[w][2];
@@ -1265,7 +1276,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   __syncthreads();
   if (!s_last) return;
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-  for (unsigned int b2 = threadIdx.x; b2 < gridDim.x; b2 += kThreads) {
+  for (unsigned int b2 = threadIdx.x; b2 < gridDim.x; b2 += kGThreads) {
     u0 += __ldcg(bp + 3 * b2);
     u1 += __ldcg(bp + 3 * b2 + 1);
     u2 += __ldcg(bp + 3 * b2 + 2);
@@ -1286,7 +1297,7 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
   if (threadIdx.x == 0) {
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) {
+    for (int w = 0; w < kGThreads / 32; ++w) {
       v0 += s_part[w][0];
       v1 += s_part[w][1];
       v2 += s_part[w][2];
@@ -1399,8 +1410,8 @@ bool setup_pass(Pass<TS, TC>& P, Carver& c, const mfg_layout* lay, int k, bool a
 }
 
 
-// CTAs of the grouped kernel: one per kThreads/8 workers of each pass.
-int grouped_blocks(int nchunks) { return (nchunks + kThreads / 8 - 1) / (kThreads / 8); }
+// CTAs of the grouped kernel: one per kGThreads/8 workers of each pass.
+int grouped_blocks(int nchunks) { return (nchunks + kGThreads / 8 - 1) / (kGThreads / 8); }
 int grouped_grid(int n0, int n1) {
   const int g = grouped_blocks(n0) + grouped_blocks(n1);
   return g < 1 ? 1 : g;
@@ -1414,7 +1425,7 @@ int launch_grouped(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int k, int kp
   if (grid != nb0 + nb1) return MFG_ERR_ARG;  // empty passes are not launched here
   const int V = kp / 8;
   constexpr bool f32 = sizeof(TS) == 4, mixed = sizeof(TS) != sizeof(TC);
-  auto go = [&](auto kern) { kern<<<grid, kThreads, 0, stream>>>(P0, P1, nb0, nb1, k, kp, F); };
+  auto go = [&](auto kern) { kern<<<grid, kGThreads, 0, stream>>>(P0, P1, nb0, nb1, k, kp, F); };
   if constexpr (f32 && !mixed) {
     if (V == 4) go(k_sweep_g8f<TS, TC, 4>);
     else go(k_sweep_g8f<TS, TC, 8>);
@@ -1484,7 +1495,7 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
     P1.out = (TS*)RtW; P1.ldout = k; P1.out_scale = out_scale; P1.want_sq = 0;
     SumJob J{};
     {
-      const size_t gb = grouped ? (size_t)grouped_grid(P0.nchunks, P1.nchunks) * (3 + 3 * (kThreads / 32)) : 0;
+      const size_t gb = grouped ? (size_t)grouped_grid(P0.nchunks, P1.nchunks) * (3 + 3 * (kGThreads / 32)) : 0;
       J.block_part = c.take<double>(gb > (size_t)kEpiBlocksMax * 5 ? gb : (size_t)kEpiBlocksMax * 5);
     }
     J.counter = c.take<unsigned int>(1);
@@ -1594,7 +1605,7 @@ size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
   carve_epi(s);
   const int64_t g = grouped_grid(chunks_of_g(csr->nnz, pick_cb_g(csr->nnz)),
                                  chunks_of_g(csc->nnz, pick_cb_g(csc->nnz)));
-  s.take<double>((size_t)g * (3 + 3 * (kThreads / 32)));
+  s.take<double>((size_t)g * (3 + 3 * (kGThreads / 32)));
   return s.off + 1024;
 }
 
