@@ -52,6 +52,8 @@ def parse():
                     help="bounded CPU-baseline sample (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tto", action="store_true", help="skip the time-to-objective leg")
+    ap.add_argument("--sweep", default="grouped", choices=["grouped", "staged"],
+                    help="sweep kernel: all-gather grouped (k_sweep_g8f) or shared-memory staged")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
                     help="L2 flush between steps: write (zero 512 MiB), read (sum 512 MiB) or none")
     return ap.parse_args()
@@ -267,7 +269,10 @@ def main():
     k = spec.k0
     obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
     w_np, h_np = synth.sweep_factors(m, n, k, seed=1 + rank, dtype=np.float32)
-    plan = SweepPlan(obs, k, compute_f64=False)
+    t_plan = time.perf_counter()
+    plan = SweepPlan(obs, k, compute_f64=False, staged=args.sweep == "staged")
+    torch.cuda.synchronize()
+    t_plan = time.perf_counter() - t_plan
     # resident factors in the grouped kernel layout (unpadded when k allows)
     w = plan.pad(torch.as_tensor(w_np, device=dev))
     h = plan.pad(torch.as_tensor(h_np, device=dev))
@@ -426,14 +431,17 @@ def main():
                           "read": "flushed before every step (512 MiB read)",
                           "none": "not flushed (L2-warm)"}[args.flush],
                    "timing": "per-step CUDA events, CUDA-graph replay of the sweep",
-                   "parallelism": f"{world} independent partitions (one per GPU)"},
+                   "parallelism": f"{world} independent partitions (one per GPU)",
+                   "sweep": args.sweep, "plan_seconds": round(t_plan, 3),
+                   **({"staged": plan.staged.stats()} if plan.staged is not None else {})},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int((m + n) * k * 4),
                 "d2h_bytes_per_step": int(plan._host.numel())},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_sweep (fused CSR+CSC pass)",
+                     "kernel": ("k_sweep_g8f (fused CSR+CSC pass)" if plan.staged is None else
+                                "k_sweep_staged + k_staged_fold (timed together)"),
                      "bytes_per_launch": kb, "avg_launch_us": kern_ms * 1e3,
                      "peak_source": peak_src,
                      "survey_unfused_bytes": survey_bytes(obs.size, m, n, k, 4)},

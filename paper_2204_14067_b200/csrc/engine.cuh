@@ -29,4 +29,15 @@ int bcd_dispatch(int dtype, const mfg_layout* lay, int k, const void* vals, cons
                  int ldo, double lam, void* out, int ldout, void* ws, size_t wsb,
                  cudaStream_t stream);
 
+// CUDA-event timing of the dominant kernel(s) (mfg_profile_enable)
+void prof_begin(cudaStream_t s);
+void prof_end(cudaStream_t s);
+
+int staged_block_rows(int k);
+int staged_workers(int k);
+size_t staged_workspace(const mfg_staged_plan* pl);
+int staged_sweep(const mfg_staged_plan* pl, const float* W, int ldw, const float* H, int ldh,
+                 float* R, float* RH, float* RtW, double out_scale, double* sums, void* ws,
+                 size_t wsb, cudaStream_t stream);
+
 }  // namespace mfg

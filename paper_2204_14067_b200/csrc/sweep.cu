@@ -39,6 +39,10 @@
 #endif
 
 #include "common.cuh"
+
+#ifndef MFG_UNROLL_U
+#define MFG_UNROLL_U 0  // unroll the 4 group-batches of a ring block
+#endif
 #include "engine.cuh"
 
 namespace mfg {
@@ -55,10 +59,10 @@ struct KernelProfiler {
 KernelProfiler g_prof;
 long long* g_probe = nullptr;  // device buffer for per-worker clock stamps (diagnostics)
 
-static void prof_begin(cudaStream_t s) {
+void prof_begin(cudaStream_t s) {
   if (g_prof.on && g_prof.used < g_prof.start.size()) cudaEventRecord(g_prof.start[g_prof.used], s);
 }
-static void prof_end(cudaStream_t s) {
+void prof_end(cudaStream_t s) {
   if (g_prof.on && g_prof.used < g_prof.start.size()) {
     cudaEventRecord(g_prof.stop[g_prof.used], s);
     ++g_prof.used;
@@ -884,6 +888,9 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
     if (left < 32) m &= left <= 0 ? 0u : ((1u << left) - 1u);
     if (b == 0) m &= ~1u;
     const int slot = b & 1;
+#if MFG_UNROLL_U
+#pragma unroll
+#endif
     for (int u = 0; u < 4; ++u) {
       const int o = b * 32 + u * 8;
       const uint32_t bits = (m >> (8 * u)) & 0xFFu;

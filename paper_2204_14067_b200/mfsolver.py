@@ -79,7 +79,8 @@ class SweepPlan:
     the BASELINE metric."""
 
     def __init__(self, obs: ObservationSet, k: int, *, want_r=True, want_rh=True, want_rtw=True,
-                 out_scale: float = 1.0, compute_f64: bool = False):
+                 out_scale: float = 1.0, compute_f64: bool = False, staged: bool = False,
+                 staged_opts: dict | None = None):
         self.obs = obs
         dev = obs.dev
         dt = obs.dtype
@@ -104,6 +105,18 @@ class SweepPlan:
         self.kp = grouped_width(self.k, dt, compute_f64)
         self.ld = grouped_ld(self.k, dt, compute_f64) or self.k
         self._host = None
+        # the shared-memory staged sweep (csrc/staged.cu): fp32, k <= 64, all outputs
+        self.staged = None
+        if staged:
+            from .staged import StagedPlan
+            if dt != torch.float32 or compute_f64 or not (want_rh and want_rtw) or self.k > 64:
+                raise ValueError("the staged sweep needs fp32 storage and arithmetic, k <= 64 "
+                                 "and both R.H and R^T.W")
+            if self.ld % 4:
+                self.ld = self.kp
+            self.staged = StagedPlan(obs, self.k, want_r=want_r, **(staged_opts or {}))
+            self.wsb = self.staged.workspace_bytes()
+            self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
 
     def pad(self, f: torch.Tensor) -> torch.Tensor:
         """Factor in the grouped kernel's layout: contiguous (rows x k) when
@@ -125,6 +138,12 @@ class SweepPlan:
 
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
         """w, h: (rows x ld) with ld = k, or the zero-padded width ``kp``."""
+        if self.staged is not None:
+            _lib.check(_lib.lib().mfg_sweep_staged(
+                self.staged.ref, w.data_ptr(), int(w.stride(0)), h.data_ptr(), int(h.stride(0)),
+                _lib.ptr(self.R), self.RH.data_ptr(), self.RtW.data_ptr(), self.out_scale,
+                self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, _lib.stream_ptr()), "staged sweep")
+            return
         _lib.check(_lib.lib().mfg_sweep(*self._args(w, h, _lib.stream_ptr())), "sweep")
 
     def run_host(self, w_host: torch.Tensor, h_host: torch.Tensor):
@@ -161,6 +180,11 @@ class SweepPlan:
                 self._wd.data_ptr(), self.ld, self._hd.data_ptr(), self.ld, _lib.ptr(self.R),
                 self._out.data_ptr(), self._host.data_ptr(), self.out_scale, self.ws.data_ptr(),
                 self.wsb, stream)
+        if self.staged is not None:
+            _lib.check(_lib.lib().mfg_sweep_staged_host(
+                self.staged.ref, w_host.data_ptr(), h_host.data_ptr(), *self._host_tail),
+                "staged sweep_host")
+            return self._host_views
         _lib.check(_lib.lib().mfg_sweep_host(*self._host_args, w_host.data_ptr(), h_host.data_ptr(),
                                              *self._host_tail), "sweep_host")
         return self._host_views
