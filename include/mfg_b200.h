@@ -188,6 +188,8 @@ typedef struct {
   const int32_t* tiles;     /* [ntiles][4] pass, block (-1 cold), chunk begin, end;
                                end - begin <= mfg_staged_workers(k)           */
   const int32_t* tile_nblk; /* [ntiles] 32-entry blocks per chunk               */
+  int32_t l1;               /* 1: L1-blocked plan (block-ordered stream, nothing
+                               staged: every tile gathers through L1)         */
 } mfg_staged_plan;
 
 /* rows of a staged block for width k (0 if k is not supported: k > 64)      */

@@ -75,6 +75,7 @@ class StagedPlanC(ctypes.Structure):
         ("chunks", ctypes.c_void_p),
         ("tiles", ctypes.c_void_p),
         ("tile_nblk", ctypes.c_void_p),
+        ("l1", ctypes.c_int32),
     ]
 
 

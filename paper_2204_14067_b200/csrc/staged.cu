@@ -590,7 +590,8 @@ int staged_sweep(const mfg_staged_plan* pl, const float* W, int ldw, const float
   MFG_REQUIRE(!R || pl->pass[0].spos, "staged sweep: R requested from a plan built without positions");
   MFG_REQUIRE(pl->grid >= 1 && pl->grid <= 4 * kNumSMs, "staged sweep: bad grid");
   const int S = staged_block_rows(k);
-  MFG_REQUIRE(pl->pass[0].S >= 1 && pl->pass[0].S <= S && pl->pass[1].S >= 1 && pl->pass[1].S <= S,
+  MFG_REQUIRE(pl->pass[0].S >= 1 && pl->pass[1].S >= 1 &&
+                  (pl->l1 || (pl->pass[0].S <= S && pl->pass[1].S <= S)),
               "staged sweep: block rows exceed the shared-memory capacity for this k");
   const int rbe = row_bytes(k) / 4;
   Carver c(ws, wsb);
@@ -625,9 +626,15 @@ int staged_sweep(const mfg_staged_plan* pl, const float* W, int ldw, const float
   A.block_part = bp;
   A.counter = counter;
   A.sums = tmp;
-  const int smem = kSmemDyn;
+  // nothing staged (L1-blocked plans): request only the rings, so the SM's
+  // unified L1/shared storage is left to the L1 cache
+  bool any_staged = false;
+  for (int t = 0; t < 2; ++t) any_staged |= pl->pass[t].nblocks > 0 && !pl->l1;
+  const int smem = any_staged ? kSmemDyn : (k <= 32 ? s_smem_fixed<4>() : s_smem_fixed<8>());
   auto go = [&](auto kern) -> int {
     MFG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        any_staged ? 100 : 0));
     kern<<<pl->grid, k <= 32 ? s_threads<4>() : s_threads<8>(), smem, stream>>>(A);
     MFG_LAUNCH_CHECK();
     return MFG_OK;

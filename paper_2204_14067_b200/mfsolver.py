@@ -146,20 +146,26 @@ class SweepPlan:
             return
         _lib.check(_lib.lib().mfg_sweep(*self._args(w, h, _lib.stream_ptr())), "sweep")
 
-    def run_host(self, w_host: torch.Tensor, h_host: torch.Tensor):
+    def run_host(self, w_host: torch.Tensor, h_host: torch.Tensor, *, graph: bool = True):
         """End-to-end sweep from host factors through one ABI call
         (mfg_sweep_host): H2D of W and H into resident device factors, the
         sweep, and one D2H of the packed results [sums | RH | RtW]. Host
         factors are contiguous (rows x k) CPU tensors, pinned for the copies
         to be asynchronous. Returns pinned host views (sums, RH, RtW), valid
-        once the current stream reaches this point and until the next call."""
+        once the current stream reaches this point and until the next call.
+
+        With ``graph`` (default) the call is captured once per (host buffers,
+        stream) into a CUDA graph -- H2D copies, sweep kernels and D2H copy as
+        one graph -- and replayed, so a step costs one graph launch on the
+        host instead of the copy and kernel enqueues. The buffers' contents
+        are read at replay time, as with the eager call."""
         if self.RH is None or self.RtW is None:
             raise ValueError("run_host needs a plan with want_rh and want_rtw")
         for t, rows in ((w_host, self.obs.m), (h_host, self.obs.n)):
             if t.device.type != "cpu" or t.dtype != self.dt or tuple(t.shape) != (rows, self.k) \
                     or not t.is_contiguous():
                 raise ValueError(f"host factor must be a contiguous CPU ({rows} x {self.k}) {self.dt} tensor")
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = torch.cuda.current_stream()
         if self._host is None:
             dev = self.obs.dev.device
             self._wd = torch.zeros((self.obs.m, self.ld), dtype=self.dt, device=dev)
@@ -169,25 +175,39 @@ class SweepPlan:
             self._host_views = (self._host[:24].view(torch.float64),
                                 self._host[32:32 + nb_rh].view(self.dt).view(self.obs.m, self.k),
                                 self._host[32 + nb_rh:].view(self.dt).view(self.obs.n, self.k))
-            self._host_key = None
-        if self._host_key != stream:
             dev = self.obs.dev
-            self._host_key = stream
             self._host_args = (
                 _lib.dtype_code(self.dt), self.compute_f64, dev.csr.ref, dev.csc.ref, self.k,
                 dev.vals.data_ptr(), dev.vals_csc.data_ptr())
             self._host_tail = (
                 self._wd.data_ptr(), self.ld, self._hd.data_ptr(), self.ld, _lib.ptr(self.R),
                 self._out.data_ptr(), self._host.data_ptr(), self.out_scale, self.ws.data_ptr(),
-                self.wsb, stream)
+                self.wsb)
+            self._graph_key = None
+        if not graph:
+            self._host_call(w_host, h_host, stream.cuda_stream)
+            return self._host_views
+        key = (w_host.data_ptr(), h_host.data_ptr(), stream.cuda_stream)
+        if self._graph_key != key:
+            self._host_call(w_host, h_host, stream.cuda_stream)  # warm-up, eager
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._host_call(w_host, h_host, side.cuda_stream)
+            stream.wait_stream(side)
+            self._graph, self._graph_key = g, key
+        self._graph.replay()
+        return self._host_views
+
+    def _host_call(self, w_host: torch.Tensor, h_host: torch.Tensor, stream: int) -> None:
         if self.staged is not None:
             _lib.check(_lib.lib().mfg_sweep_staged_host(
-                self.staged.ref, w_host.data_ptr(), h_host.data_ptr(), *self._host_tail),
+                self.staged.ref, w_host.data_ptr(), h_host.data_ptr(), *self._host_tail, stream),
                 "staged sweep_host")
-            return self._host_views
+            return
         _lib.check(_lib.lib().mfg_sweep_host(*self._host_args, w_host.data_ptr(), h_host.data_ptr(),
-                                             *self._host_tail), "sweep_host")
-        return self._host_views
+                                             *self._host_tail, stream), "sweep_host")
 
 
 def sweep(obs: ObservationSet, wf: FactorPair, *, want_r=False, want_rh=False, want_rtw=False,

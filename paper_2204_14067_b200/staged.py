@@ -58,7 +58,8 @@ def _pack_bits(flags: torch.Tensor) -> torch.Tensor:
 class _PassPlan:
     """Streams of one orientation (see the module docstring)."""
 
-    def __init__(self, idx, rows, vals, nrows, ngath, S, lmin, want_pos, stage_min=4.0):
+    def __init__(self, idx, rows, vals, nrows, ngath, S, lmin, want_pos, stage_min=4.0,
+                 l1=False):
         dev = idx.device
         nnz = int(idx.numel())
         self.nrows, self.ngath, self.S = int(nrows), int(ngath), int(S)
@@ -99,7 +100,8 @@ class _PassPlan:
         at = start[seg_s] + within                                  # stream position of sorted entries
         L_ = self.nstream + 64
         gcol = idx64[perm]
-        slot = torch.where(seg_s < staged, rank[gcol] % S, gcol)
+        slot = gcol if l1 else torch.where(seg_s < staged, rank[gcol] % S, gcol)
+        self.l1 = l1
         self.sidx = torch.zeros(L_, dtype=torch.int32, device=dev)
         self.srow = torch.zeros(L_, dtype=torch.int32, device=dev)
         self.svals = torch.zeros(L_, dtype=torch.float32, device=dev)
@@ -137,7 +139,7 @@ class _PassPlan:
         for s, (n, e0) in enumerate(zip(self.seg_counts, self.seg_starts)):
             if n == 0:
                 continue
-            block = s if s < self.nblocks else -1
+            block = s if (s < self.nblocks and not self.l1) else -1
             t = max(1, round(n / te))
             per = -(-n // (groups * t))
             cb = max(32, -(-per // 32) * 32)
@@ -210,22 +212,31 @@ class StagedPlan:
 
     def __init__(self, obs, k: int, *, S: int | None = None, lmin: float = 8.0,
                  stage_min: float = 4.0, grid: int = NUM_SMS, tiles_per_cta: int = 4,
-                 want_r: bool = True):
+                 want_r: bool = True, l1_bytes: int = 0):
         src = obs if isinstance(obs, StagedInput) else StagedInput.of(obs)
         if src.vals.dtype != torch.float32:
             raise ValueError("the staged sweep runs on fp32 storage")
         smax = block_rows(k)
         if smax <= 0:
             raise ValueError(f"the staged sweep supports 1 <= k <= 64 (got {k})")
-        S = smax if S is None else int(S)
-        if not 1 <= S <= smax:
-            raise ValueError(f"block rows must be in [1, {smax}]")
+        # l1_bytes > 0: "L1-blocked" mode -- the same block-ordered stream, but
+        # nothing is staged: tiles of one block run back to back on an SM and
+        # its L1 caches the block's rows (gathers stay global loads)
+        l1 = l1_bytes > 0
+        if l1:
+            S = max(1, int(l1_bytes) // (((int(k) * 4 + 15) // 16) * 16)) if S is None else int(S)
+        else:
+            S = smax if S is None else int(S)
+            if not 1 <= S <= smax:
+                raise ValueError(f"block rows must be in [1, {smax}]")
+        self.l1 = l1
         self.k, self.S, self.grid = int(k), S, int(grid)
         self.m, self.n = src.m, src.n
         nnz = src.nnz
         self.p = [
-            _PassPlan(src.csr_idx, src.csr_row, src.vals, src.m, src.n, S, lmin, want_r, stage_min),
-            _PassPlan(src.csc_idx, src.csc_row, src.vals_csc, src.n, src.m, S, lmin, False, stage_min),
+            _PassPlan(src.csr_idx, src.csr_row, src.vals, src.m, src.n, S, lmin, want_r, stage_min, l1),
+            _PassPlan(src.csc_idx, src.csc_row, src.vals_csc, src.n, src.m, S, lmin, False, stage_min,
+                      l1),
         ]
         total = 2 * nnz
         self.groups = G = workers(k)
@@ -250,7 +261,7 @@ class StagedPlan:
         self.c = _lib.StagedPlanC((_lib.StagedPass * 2)(self.p[0].cstruct(), self.p[1].cstruct()),
                                   self.k, self.grid, len(chunks), len(tiles),
                                   self.chunks.data_ptr(), self.tiles.data_ptr(),
-                                  self.tile_nblk.data_ptr())
+                                  self.tile_nblk.data_ptr(), 1 if self.l1 else 0)
 
     @property
     def ref(self):
@@ -263,7 +274,9 @@ class StagedPlan:
             "staged_frac": [pp.entries_staged / max(pp.nnz, 1) for pp in self.p],
             "pieces": [pp.npieces for pp in self.p],
             "tiles": self.ntiles,
+            "mode": "l1-blocked" if self.l1 else "smem-staged",
         }
 
     def workspace_bytes(self) -> int:
         return int(_lib.lib().mfg_sweep_staged_workspace(self.ref))
+

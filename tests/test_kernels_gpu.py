@@ -241,14 +241,24 @@ def test_grouped_sweep_vs_oracle(k, dtype, layout):
     R0, RH0 = plan.R.clone(), plan.RH.clone()
     plan.run(plan.pad(wt), plan.pad(ht))
     assert torch.equal(R0, plan.R) and torch.equal(RH0, plan.RH)
-    # end-to-end entry point from host factors: same results
-    sums_h, rh_h, rtw_h = plan.run_host(torch.as_tensor(w).to(dtype).pin_memory(),
-                                        torch.as_tensor(h).to(dtype).pin_memory())
+    # end-to-end entry point from host factors: same results, eager and as a
+    # replayed CUDA graph (which reads the host buffers at replay time)
+    RtW0 = plan.RtW.clone()
+    wh = torch.as_tensor(w).to(dtype).pin_memory()
+    hh = torch.as_tensor(h).to(dtype).pin_memory()
+    for graph in (False, True, True):
+        sums_h, rh_h, rtw_h = plan.run_host(wh, hh, graph=graph)
+        torch.cuda.synchronize()
+        assert torch.equal(rh_h, RH0.cpu()) and torch.equal(rtw_h, RtW0.cpu())
+        sh = sums_h.numpy()
+        assert sh[0] == sums[0]                              # same per-entry order
+        assert np.allclose(sh[1:], sums[1:], rtol=1e-13)     # norms: layout-dependent slices
+    wh.mul_(0.5)   # new contents in the same pinned buffers -> the graph sees them
+    sums_h, rh_h, _ = plan.run_host(wh, hh)
     torch.cuda.synchronize()
-    assert torch.equal(rh_h, RH0.cpu()) and torch.equal(rtw_h, plan.RtW.cpu())
-    sh = sums_h.numpy()
-    assert sh[0] == sums[0]                              # same per-entry order
-    assert np.allclose(sh[1:], sums[1:], rtol=1e-13)     # norms: layout-dependent slices
+    rr2, rh2, _, sq2, _, _ = orc.sweep(om, _np(wt) * 0.5, _np(ht))
+    assert np.max(np.abs(rh_h.double().numpy() - rh2)) <= tol * amp * sc(rh2)
+    assert sums_h.numpy()[0] == pytest.approx(sq2, rel=tol * 10)
 
 
 @pytest.mark.parametrize("k", [130, 150, 200])

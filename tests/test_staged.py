@@ -141,7 +141,8 @@ def _gpu_obs(m, n, rows, cols, vals):
 @pytest.mark.gpu
 @pytest.mark.parametrize("k", [1, 3, 8, 20, 30, 32, 40, 64])
 @pytest.mark.parametrize("opts", [{}, {"S": 9, "lmin": 3.0, "stage_min": 0.5},
-                                  {"S": 4, "lmin": 1e9}, {"S": 5, "lmin": 1.0, "stage_min": 0.0}])
+                                  {"S": 4, "lmin": 1e9}, {"S": 5, "lmin": 1.0, "stage_min": 0.0},
+                                  {"l1_bytes": 2048, "lmin": 2.0, "stage_min": 0.5}])
 def test_staged_sweep_matches_oracle(k, opts):
     from paper_2204_14067_b200 import mfsolver as MF
     m, n, rows, cols, vals = _zipf_instance(7 + k, 90, 130, 3000)
@@ -152,6 +153,8 @@ def test_staged_sweep_matches_oracle(k, opts):
     h = rng.standard_normal((n, k)).astype(np.float32)
     if "S" in opts:
         opts = dict(opts, S=min(opts["S"], ST.block_rows(k)))
+    if "l1_bytes" in opts and k > 32:
+        opts = dict(opts, l1_bytes=4096)
     plan = MF.SweepPlan(obs, k, staged=True, staged_opts=opts)
     wd = plan.pad(torch.from_numpy(w).cuda())
     hd = plan.pad(torch.from_numpy(h).cuda())
@@ -204,3 +207,23 @@ def test_staged_sweep_matches_grouped_sweep_c2_scale():
     sums, RH, RtW = b.run_host(wh, hh)
     torch.cuda.synchronize()
     assert torch.equal(RH, b.RH.cpu()) and torch.equal(RtW, b.RtW.cpu())
+
+
+def test_plan_walk_l1_blocked_matches_oracle():
+    """L1-blocked plans: block-ordered stream, every tile gathers globally."""
+    m, n, rows, cols, vals = _zipf_instance(6, 40, 60, 700)
+    om, src = _input_cpu(m, n, rows, cols, vals)
+    rng = rng_for(106)
+    k = 6
+    w = rng.standard_normal((m, k)).astype(np.float32).astype(np.float64)
+    h = rng.standard_normal((n, k)).astype(np.float32).astype(np.float64)
+    plan = ST.StagedPlan(src, k, S=5, lmin=2.0, stage_min=0.5, grid=5, l1_bytes=1)
+    assert plan.stats()["mode"] == "l1-blocked" and max(plan.stats()["blocks"]) > 1
+    assert (plan.tiles.numpy()[:, 1] == -1).all()
+    R, RH, RtW, sq = _simulate(plan, w, h)
+    rr, rh, rtw, sq0, _, _ = orc.sweep(om, w, h)
+    np.testing.assert_allclose(R, rr, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(RH, rh, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(RtW, rtw, rtol=0, atol=1e-11)
+    assert abs(sq - sq0) <= 1e-12 * sq0
+

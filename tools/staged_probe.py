@@ -27,7 +27,10 @@ def run(args):
     w_np, h_np = synth.sweep_factors(m, n, k, seed=1, dtype=np.float32)
     flush = torch.zeros(512 << 20, dtype=torch.uint8, device="cuda")
     out = {}
-    for name, kw in [("grouped", {}), ("staged", {"staged": True, "staged_opts": {"lmin": args.lmin, "tiles_per_cta": args.tpc}})]:
+    variants = [("grouped", {}),
+                ("staged", {"staged": True, "staged_opts": {"lmin": args.lmin, "tiles_per_cta": args.tpc,
+                                                            "l1_bytes": args.l1}})]
+    for name, kw in variants:
         plan = SweepPlan(obs, k, compute_f64=False, **kw)
         w = plan.pad(torch.as_tensor(w_np, device="cuda"))
         h = plan.pad(torch.as_tensor(h_np, device="cuda"))
@@ -51,4 +54,5 @@ if __name__ == "__main__":
     ap.add_argument("--lmin", type=float, default=4.0)
     ap.add_argument("--tpc", type=int, default=2)
     ap.add_argument("--tag", default="full")
+    ap.add_argument("--l1", type=int, default=0, help="L1-blocked mode with this many bytes per block")
     run(ap.parse_args())
