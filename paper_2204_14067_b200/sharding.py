@@ -130,7 +130,10 @@ class ShardedMF:
       ops.half_sweep(handle, other_full, lam) -> new self rows
       ops.residual(handle, self_rows, other_full) -> r values (handle order)
       ops.spmm(handle, vals, block_full) -> rows sum_j vals_ij block_j
-    (the last two serve the sharded lifting step, ``sharded_lift``).
+      ops.sddmm_sums(handle, left_rows, right_full, scale, g, with_a) -> fp64
+          (sum r^2, sum g (r - g/2), sum g p)
+    (the last three serve the sharded lifting step and driver,
+    ``sharded_lift`` / ``sharded_solver``).
     """
 
     def __init__(self, shard: Shard, ops, comm: Comm, device):
@@ -200,12 +203,23 @@ class DeviceOps:
         return _half_sweep(obs, False, other_full, lam)
 
     def residual(self, obs, self_rows, other_full):
-        """r on the shard (fp64, the handle's CSR order): self_i . other_j - a_ij."""
+        """r on the shard (fp64, the handle's CSR order): self_i . other_j - a_ij.
+        Factors stored in fp32 convert to fp64 exactly; fp64 blocks (SVD
+        triplets of the lifting step) are used at full precision."""
         from .data import sddmm
 
-        vals, _ = sddmm(obs, self_rows.to(obs.dtype).double(), other_full.to(obs.dtype).double(),
-                        dtype=torch.float64)
+        vals, _ = sddmm(obs, self_rows.double(), other_full.double(), dtype=torch.float64)
         return vals
+
+    def sddmm_sums(self, obs, left_rows, right_full, scale, g_vals, with_a=True):
+        """fp64 (sum r^2, sum g (r - g/2), sum g p) with p_ij = left_i diag(scale)
+        right_j and r = p - a (r = p without a) over the shard (mfg_sddmm)."""
+        from .data import sddmm
+
+        sc = None if scale is None else torch.as_tensor(scale).double().cpu().numpy()
+        _, sums = sddmm(obs, left_rows.double(), right_full.double(), scale=sc, a=with_a,
+                        g=g_vals.double(), want_out=False, dtype=torch.float64)
+        return float(sums[0]), float(sums[1]), float(sums[2])
 
     def spmm(self, obs, vals, block_full):
         """sum_j vals_ij block_j for the shard's rows (fp64, libmfg_b200 mfg_spmm)."""

@@ -356,6 +356,28 @@ def gen_traces():
         json.dump(out, fh)
 
 
+def gen_traces_estimated():
+    """Solver traces with the estimated certification mode (the only mode of
+    the sharded driver), for the sharded-solver parity tests."""
+    out = {}
+    runs = [("mfg_est_planted3", planted(3, 30, 36, 3, 0.5, 0.05),
+             dict(lam=2.0, k0=4, max_outer_iters=12, seed=3, cert_mode="estimated")),
+            ("mfg_est_crit4", planted(2024, 100, 120, 5, 0.3, 0.1),
+             dict(lam=8.0, k0=8, max_outer_iters=10, seed=7, cert_mode="estimated"))]
+    for name, obs, kw in runs:
+        cfg = rdrv.SolverConfig(**kw)
+        t0 = time.perf_counter()
+        x, _, tr = rdrv.solve_mf_global(obs, None, cfg)
+        el = time.perf_counter() - t0
+        d = trace_dict(tr)
+        d.update(kind="mf_global", cfg=kw, m=obs.m, n=obs.n, rows=obs.rows.tolist(),
+                 cols=obs.cols.tolist(), vals=obs.vals.tolist(), elapsed_s=el)
+        out[name] = d
+        print(name, len(tr), "iters", f"{el:.1f}s", "final rank", d["rank"][-1], "obj", d["obj"][-1])
+    with open(os.path.join(HERE, "traces_estimated.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 def gen_c1():
     m, n, r, c, v = synth.generate("c1")
     m, n, r, c, v, tr = synth.canonical(m, n, r, c, v)
@@ -377,6 +399,9 @@ if __name__ == "__main__":
     print("reference", mfglobal.__version__, "numpy", np.__version__)
     if "--c1" in sys.argv:
         gen_c1()
+        sys.exit(0)
+    if "--estimated" in sys.argv:
+        gen_traces_estimated()
         sys.exit(0)
     gen_omega()
     gen_sweep()
