@@ -1,0 +1,99 @@
+"""Sweep parity at BASELINE.json's full sizes (c3: 10M entries, c4: 100M; c5
+with MFG_TEST_C5=1) through size-independent properties, since the CPU
+oracle cannot run a full c4 sweep in test time:
+
+* adjointness: <R.H, W> = <R^T.W, H> = sum_e r_e (r_e + a_e) (the three
+  contractions of the same residual; fp32 outputs, fp64 sums: 1e-4 rel);
+* the fused sum r^2 against the stored R (1e-5 rel);
+* sampled exactness: 4096 random entries' residuals (2e-5 of the scale, the
+  fp32 sweep tolerance) and 32 random rows each of R.H and R^T.W recomputed
+  in fp64 from the same fp32 inputs (within the forward-error bound of an
+  fp32 accumulation, ``_fp32_sum_bound``);
+* Omega index handling: CSR rows sorted, CSC order = stable argsort of the
+  columns (bit-exact), and bitwise run-to-run determinism of the sweep.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+WORKLOADS = ["c3", "c4"] + (["c5"] if os.environ.get("MFG_TEST_C5") else [])
+
+
+def _fp32_sum_bound(terms, ref_row) -> float:
+    """Forward-error bound of an fp32 accumulation of ``terms`` (per dim):
+    1e-5 * sum |term| (~170 fp32 ulps of the absolute sum) + 2e-5 * |result|."""
+    return float((1e-5 * terms.abs().sum(0) + 2e-5 * ref_row.abs()).max()) + 1e-6
+
+
+@pytest.mark.parametrize("wl", WORKLOADS)
+def test_full_size_sweep_properties(wl):
+    from paper_2204_14067_b200 import synth
+    from paper_2204_14067_b200.data import ObservationSet
+    from paper_2204_14067_b200.mfsolver import SweepPlan
+
+    m, n, r, c, v = synth.generate(wl, seed=0)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    k = synth.CONFIGS[wl].k0
+    obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
+    w_np, h_np = synth.sweep_factors(m, n, k, seed=5, dtype=np.float32)
+    plan = SweepPlan(obs, k, compute_f64=False)
+    w = plan.pad(torch.as_tensor(w_np, device="cuda"))
+    h = plan.pad(torch.as_tensor(h_np, device="cuda"))
+    plan.run(w, h)
+    torch.cuda.synchronize()
+    R = plan.R.double()
+    A = obs.dev.vals64[: obs.size]
+    RH, RtW = plan.RH.double(), plan.RtW.double()
+    W64 = torch.as_tensor(w_np, device="cuda").double()
+    H64 = torch.as_tensor(h_np, device="cuda").double()
+    # adjointness of the three contractions of R
+    a1 = float((RH * W64).sum())
+    a2 = float((RtW * H64).sum())
+    a3 = float((R * (R + A)).sum())
+    assert a1 == pytest.approx(a3, rel=1e-4) and a2 == pytest.approx(a3, rel=1e-4)
+    # the fused fp64 sum r^2 and the norms
+    s = plan.sums.cpu().numpy()
+    assert s[0] == pytest.approx(float((R * R).sum()), rel=1e-5)
+    assert s[1] == pytest.approx(float((W64 * W64).sum()), rel=1e-12)
+    assert s[2] == pytest.approx(float((H64 * H64).sum()), rel=1e-12)
+    # sampled entries, exact in fp64 from the fp32 inputs
+    rng = np.random.default_rng(7)
+    d = obs.dev
+    rows = d.csr.row_of[: obs.size]
+    cols = d.csr.idx[: obs.size]
+    e = torch.as_tensor(rng.integers(0, obs.size, 4096), device="cuda")
+    ri, ci = rows[e].long(), cols[e].long()
+    ref = (W64[ri] * H64[ci]).sum(1) - A[e]
+    scale = float(ref.abs().max()) + 1.0
+    assert float((R[e] - ref).abs().max()) <= 2e-5 * scale
+    # sampled rows of R.H and R^T.W
+    ptr = d.csr.ptr.long()
+    for i in rng.integers(0, m, 32):
+        lo, hi = int(ptr[i]), int(ptr[i + 1])
+        terms = R[lo:hi, None] * H64[cols[lo:hi].long()]
+        ref_row = terms.sum(0)
+        assert float((RH[i] - ref_row).abs().max()) <= _fp32_sum_bound(terms, ref_row)
+    cptr = d.csc.ptr.long()
+    perm = d.csc_perm.long()
+    for j in rng.integers(0, n, 32):
+        lo, hi = int(cptr[j]), int(cptr[j + 1])
+        pos = perm[lo:hi]
+        terms = R[pos, None] * W64[rows[pos].long()]
+        ref_row = terms.sum(0)
+        assert float((RtW[j] - ref_row).abs().max()) <= _fp32_sum_bound(terms, ref_row)
+    # index handling: CSR sorted by (row, col); CSC = stable argsort of cols
+    key = rows.long() * n + cols.long()
+    assert bool((key[1:] > key[:-1]).all())
+    assert torch.equal(perm, torch.sort(cols.long(), stable=True).indices)
+    assert torch.equal(d.csc.idx[: obs.size].long(), rows.long()[perm])
+    # bitwise determinism
+    R0, RH0, RtW0, s0 = plan.R.clone(), plan.RH.clone(), plan.RtW.clone(), plan.sums.clone()
+    plan.run(w, h)
+    torch.cuda.synchronize()
+    assert torch.equal(R0, plan.R) and torch.equal(RH0, plan.RH) and torch.equal(RtW0, plan.RtW)
+    assert torch.equal(s0, plan.sums)
