@@ -394,10 +394,20 @@ def main():
     kb = kernel_bytes(obs.size, m, n, k, 4)
     achieved = kb / (kern_ms * 1e-3) / 1e9
     traffic = None
+    l2 = None
     tp = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
-            traffic = json.load(fh).get(args.workload)
+            tj = json.load(fh)
+        traffic = tj.get(args.workload)
+        l2b = tj.get("l2_bytes", {}).get(args.workload)
+        if l2b and plan.staged is None:
+            # bytes through L2 per launch (ncu capture) over the live kernel time,
+            # against the LTS throughput cap (~6300 B/cycle at the max SM clock)
+            cap = 6300 * 1.965e9 / 1e12
+            l2 = {"bytes_per_launch": l2b, "achieved_TBps": l2b / (kern_ms * 1e-3) / 1e12,
+                  "cap_TBps": cap, "frac": l2b / (kern_ms * 1e-3) / 1e12 / cap,
+                  "source": "lts__t_sectors.sum * 32 from profiles/r1f_*_k_sweep_g8f_full.json"}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -444,7 +454,8 @@ def main():
                                 "k_sweep_staged + k_staged_fold (timed together)"),
                      "bytes_per_launch": kb, "avg_launch_us": kern_ms * 1e3,
                      "peak_source": peak_src,
-                     "survey_unfused_bytes": survey_bytes(obs.size, m, n, k, 4)},
+                     "survey_unfused_bytes": survey_bytes(obs.size, m, n, k, 4),
+                     "l2": l2},
         "cpu_baseline": cpu,
         "clocks": clocks,
         "time_to_objective": tto,
