@@ -40,6 +40,10 @@
 
 #include "common.cuh"
 
+#ifndef MFG_SMEM_REDUCE
+#define MFG_SMEM_REDUCE 1  // fp32: partial-dot transpose through shared memory instead of the
+                           // butterfly (11 fewer instructions per batch; c3/c4 -1.4%)
+#endif
 #ifndef MFG_UNROLL_U
 #define MFG_UNROLL_U 0  // unroll the 4 group-batches of a ring block
 #endif
@@ -960,7 +964,21 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
         p[i] = dotv<TS, TC, V>(w, h[i]);
       }
     }
-    const TC dot = reduce8(p);
+    TC dot;
+    if constexpr (MFG_SMEM_REDUCE && sizeof(TC) == 4) {
+      // transpose through shared memory: lane q writes its partials of the 8
+      // entries down column q, then sums row q (entry q) in fixed order
+      TC* s_p = s_r + 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s_p[i * 8 + q] = p[i];
+      __syncwarp();
+      TC t[8];
+      ld4<TC>(s_p + q * 8, *reinterpret_cast<TC(*)[4]>(&t[0]));
+      ld4<TC>(s_p + q * 8 + 4, *reinterpret_cast<TC(*)[4]>(&t[4]));
+      dot = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+    } else {
+      dot = reduce8(p);
+    }
     const TC r = valid ? dot - a : TC(0);
     if (valid) {
       if (P.R) P.R[E0 + o + q] = (TS)r;
@@ -1190,7 +1208,8 @@ __global__ void __launch_bounds__(kGThreads, g8_min_blocks<TS, TC, V>())
 k_sweep_g8f(Pass<TS, TC> P0, Pass<TS, TC> P1, int nb0, int nb1, int k, int kp, FusedRed F) {
   __shared__ __align__(16) int32_t s_ring[kGThreads / 8][128];   // [cols|rows][2 slots][32]
   __shared__ __align__(16) TS s_vring[kGThreads / 8][64];        // [2 slots][32]
-  __shared__ __align__(16) TC s_r[kGThreads / 8][8];
+  // per worker: r of the batch [8] (+ the 8 x 8 partial-dot transpose)
+  __shared__ __align__(16) TC s_r[kGThreads / 8][(MFG_SMEM_REDUCE && sizeof(TC) == 4) ? 72 : 8];
   __shared__ int s_ticket;
   const int gl = threadIdx.x >> 3;
   // diagnostics: block entry stamps after the per-worker records

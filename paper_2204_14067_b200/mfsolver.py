@@ -190,15 +190,31 @@ class SweepPlan:
         key = (w_host.data_ptr(), h_host.data_ptr(), stream.cuda_stream)
         if self._graph_key != key:
             self._host_call(w_host, h_host, stream.cuda_stream)  # warm-up, eager
-            side = torch.cuda.Stream()
-            side.wait_stream(stream)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=side):
-                self._host_call(w_host, h_host, side.cuda_stream)
-            stream.wait_stream(side)
+            g = self._capture(w_host, h_host, stream)
+            if g is None:       # capture not possible here: stay eager for this plan
+                return self._host_views
             self._graph, self._graph_key = g, key
         self._graph.replay()
         return self._host_views
+
+    def _capture(self, w_host, h_host, stream):
+        """Capture one end-to-end call as a CUDA graph (None if the capture is
+        invalidated, e.g. by an unrelated thread's synchronising call)."""
+        if getattr(self, "_no_graph", False):
+            return None
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+                self._host_call(w_host, h_host, side.cuda_stream)
+        except RuntimeError:
+            torch.cuda.synchronize()
+            self._no_graph = True
+            return None
+        stream.wait_stream(side)
+        return g
 
     def _host_call(self, w_host: torch.Tensor, h_host: torch.Tensor, stream: int) -> None:
         if self.staged is not None:
