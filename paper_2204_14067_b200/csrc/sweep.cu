@@ -1550,13 +1550,12 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
       }
       FusedRed F{};
       F.W = W; F.wcount = J.wcount; F.H = H; F.hcount = J.hcount; F.is_f64 = J.is_f64;
-      F.block_part = J.block_part; F.counter = fcounter; F.sums = tmp;
+      // the last block writes [sum r^2, |W|^2, |H|^2] straight into the caller's
+      // sums (no trailing device-to-device copy node in the sweep)
+      F.block_part = J.block_part; F.counter = fcounter; F.sums = sums;
       st = launch_grouped<TS, TC>(P0, P1, k, kpg, F, stream);
       prof_end(stream);
-      if (st != MFG_OK) return st;
-      MFG_CUDA_CHECK(cudaMemcpyAsync(sums, tmp, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
-                                     stream));
-      return MFG_OK;
+      return st;
     }
     if (acc0 || acc1) st = launch_main<TS, TC, true>(P0, P1, n0, n1, k, stream);
     else st = launch_main<TS, TC, false>(P0, P1, n0, 0, k, stream);
