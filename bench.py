@@ -350,8 +350,9 @@ def main():
     # end-to-end leg through the public API (SweepPlan.run_host) with pinned
     # host factors: H2D of the step's inputs (W, H), the sweep, and one D2H of
     # the packed results [sums | RH | RtW]
-    w_host = torch.as_tensor(w_np).pin_memory()
-    h_host = torch.as_tensor(h_np).pin_memory()
+    w_host, h_host = plan.pinned_factors()
+    w_host.copy_(torch.as_tensor(w_np))
+    h_host.copy_(torch.as_tensor(h_np))
 
     def e2e_step():
         return plan.run_host(w_host, h_host)

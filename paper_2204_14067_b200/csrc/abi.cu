@@ -132,8 +132,15 @@ extern "C" int mfg_sweep_host(int dtype, int compute_f64, const mfg_layout* csr,
       return cudaMemcpyAsync(dst, src, rows * k * es, cudaMemcpyHostToDevice, st);
     return cudaMemcpy2DAsync(dst, ld * es, src, k * es, k * es, rows, cudaMemcpyHostToDevice, st);
   };
-  MFG_CUDA_CHECK(h2d(W, ldw, W_host, m));
-  MFG_CUDA_CHECK(h2d(H, ldh, H_host, n));
+  // W and H adjacent on both sides (SweepPlan.pinned_factors): one copy
+  if ((size_t)ldw == (size_t)k && (size_t)ldh == (size_t)k &&
+      static_cast<const char*>(H_host) == static_cast<const char*>(W_host) + m * k * es &&
+      static_cast<char*>(H) == static_cast<char*>(W) + m * k * es) {
+    if (m + n) MFG_CUDA_CHECK(cudaMemcpyAsync(W, W_host, (m + n) * k * es, cudaMemcpyHostToDevice, st));
+  } else {
+    MFG_CUDA_CHECK(h2d(W, ldw, W_host, m));
+    MFG_CUDA_CHECK(h2d(H, ldh, H_host, n));
+  }
   char* o = static_cast<char*>(out);
   const int rc = mfg_sweep(dtype, compute_f64, csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R,
                            o + 32, o + 32 + m * k * es, out_scale, reinterpret_cast<double*>(o),

@@ -168,8 +168,11 @@ class SweepPlan:
         stream = torch.cuda.current_stream()
         if self._host is None:
             dev = self.obs.dev.device
-            self._wd = torch.zeros((self.obs.m, self.ld), dtype=self.dt, device=dev)
-            self._hd = torch.zeros((self.obs.n, self.ld), dtype=self.dt, device=dev)
+            # W and H resident in one allocation (one H2D when the host
+            # factors are adjacent too, see pinned_factors)
+            whd = torch.zeros((self.obs.m + self.obs.n) * self.ld, dtype=self.dt, device=dev)
+            self._wd = whd[: self.obs.m * self.ld].view(self.obs.m, self.ld)
+            self._hd = whd[self.obs.m * self.ld:].view(self.obs.n, self.ld)
             self._host = torch.empty(self._out.numel(), dtype=torch.uint8).pin_memory()
             nb_rh = self.RH.numel() * self.RH.element_size()
             self._host_views = (self._host[:24].view(torch.float64),
@@ -196,6 +199,14 @@ class SweepPlan:
             self._graph, self._graph_key = g, key
         self._graph.replay()
         return self._host_views
+
+    def pinned_factors(self):
+        """Pinned host buffers (W: m x k, H: n x k) for ``run_host``, adjacent
+        in one allocation so the end-to-end call moves both with one H2D copy.
+        Fill them in place between calls."""
+        whh = torch.zeros((self.obs.m + self.obs.n) * self.k, dtype=self.dt).pin_memory()
+        return (whh[: self.obs.m * self.k].view(self.obs.m, self.k),
+                whh[self.obs.m * self.k:].view(self.obs.n, self.k))
 
     def _capture(self, w_host, h_host, stream):
         """Capture one end-to-end call as a CUDA graph (None if the capture is

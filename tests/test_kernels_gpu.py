@@ -246,6 +246,14 @@ def test_grouped_sweep_vs_oracle(k, dtype, layout):
     RtW0 = plan.RtW.clone()
     wh = torch.as_tensor(w).to(dtype).pin_memory()
     hh = torch.as_tensor(h).to(dtype).pin_memory()
+    wa, ha = plan.pinned_factors()          # adjacent buffers: the one-copy path
+    wa.copy_(wh)
+    ha.copy_(hh)
+    for wx, hx, graph in ((wh, hh, False), (wh, hh, True), (wh, hh, True), (wa, ha, False),
+                          (wa, ha, True)):
+        sums_h, rh_h, rtw_h = plan.run_host(wx, hx, graph=graph)
+        torch.cuda.synchronize()
+        assert torch.equal(rh_h, RH0.cpu()) and torch.equal(rtw_h, RtW0.cpu())
     for graph in (False, True, True):
         sums_h, rh_h, rtw_h = plan.run_host(wh, hh, graph=graph)
         torch.cuda.synchronize()
