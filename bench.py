@@ -52,6 +52,9 @@ def parse():
                     help="bounded CPU-baseline sample (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tto", action="store_true", help="skip the time-to-objective leg")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: the ranks sweep row/column shards of ONE instance "
+                         "(mfg_sweep_sharded, no data-path collective) instead of one instance each")
     ap.add_argument("--sweep", default="grouped", choices=["grouped", "staged"],
                     help="sweep kernel: all-gather grouped (k_sweep_g8f) or shared-memory staged")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
@@ -250,6 +253,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.shard:
+        main_shard(args, rank, world, local_rank)
         return
 
     import torch
@@ -462,6 +468,154 @@ def main():
         "time_to_objective": tto,
     }
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_shard(args, rank, world, local_rank):
+    """Strong scaling of one instance: rank p sweeps its row block R_p (CSR)
+    and column block C_p (CSC) with full W/H replicas (SURVEY.md §8(e));
+    R.H rows R_p and R^T.W rows C_p are final on their rank, so the data
+    path has no collective. value = whole-instance sweeps per second."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_14067_b200 import _lib, sharding, synth
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    lib = _lib.lib()
+    m, n, r, c, v, spec = instance(args.workload, seed=0)
+    k = spec.k0
+    shard = sharding.make_shard(m, n, r, c, v, rank, world)
+    r0, r1 = shard.row_block
+    c0, c1 = shard.col_block
+    ops = sharding.DeviceOps(torch.float32)
+    obs_r = ops.prepare(r1 - r0, n, shard.r_rows, shard.r_cols, shard.r_vals)
+    obs_c = ops.prepare(c1 - c0, m, shard.c_rows, shard.c_cols, shard.c_vals)
+    plan = sharding.ShardSweepPlan(shard, obs_r, obs_c, k)
+    w_np, h_np = synth.sweep_factors(m, n, k, seed=1, dtype=np.float32)
+    w = plan.pad(torch.as_tensor(w_np, device=dev))
+    h = plan.pad(torch.as_tensor(h_np, device=dev))
+    flush = torch.zeros(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    c_0 = lib.mfg_launch_count()
+    plan.run(w, h)
+    torch.cuda.synchronize()
+    launches_per_step = lib.mfg_launch_count() - c_0
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        plan.run(w, h)
+    stream.wait_stream(side)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        plan.run(w, h)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.15)
+
+    def timed(fn, steps, pre=None):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        if world > 1:
+            dist.barrier()
+        sampler.mark(t0, t1)
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        g.replay()
+    ms_total = max_over_ranks(timed(g.replay, args.steps))
+    value = args.steps / (ms_total / 1e3)
+    lib.mfg_profile_enable(args.steps)
+    timed(lambda: plan.run(w, h), args.steps)
+    tot = _lib.ctypes.c_double(0.0)
+    cnt = _lib.ctypes.c_int(0)
+    lib.mfg_profile_collect(_lib.ctypes.byref(tot), _lib.ctypes.byref(cnt))
+    lib.mfg_profile_enable(0)
+    kern_ms = tot.value / max(cnt.value, 1)
+    # end to end: H2D of the full factor replicas from pinned host memory,
+    # the shard sweep, D2H of this rank's [sums | R.H rows | R^T.W rows]
+    w_host = torch.as_tensor(w_np).pin_memory()
+    h_host = torch.as_tensor(h_np).pin_memory()
+    sums_host = torch.empty(3, dtype=torch.float64).pin_memory()
+    rh_host = torch.empty(plan.RH.shape, dtype=plan.RH.dtype).pin_memory()
+    rtw_host = torch.empty(plan.RtW.shape, dtype=plan.RtW.dtype).pin_memory()
+
+    def e2e_step():
+        w[:, :k].copy_(w_host, non_blocking=True)
+        h[:, :k].copy_(h_host, non_blocking=True)
+        plan.run(w, h)
+        sums_host.copy_(plan.sums, non_blocking=True)
+        rh_host.copy_(plan.RH, non_blocking=True)
+        rtw_host.copy_(plan.RtW, non_blocking=True)
+
+    for _ in range(min(args.warmup, 5)):
+        e2e_step()
+    e2e_ms = max_over_ranks(timed(e2e_step, args.steps))
+    e2e_value = args.steps / (e2e_ms / 1e3)
+    clocks = sampler.stop()
+    sums = plan.sums.cpu().numpy()
+    if not np.all(np.isfinite(sums)):
+        raise RuntimeError("non-finite sweep sums")
+    if rank == 0:
+        nnz_r, nnz_c = obs_r.size, obs_c.size
+        kb = int(nnz_r * 16 + nnz_c * 12 + 0.125 * (nnz_r + nnz_c)
+                 + 12 * ((r1 - r0) + (c1 - c0)) * k)
+        peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+        if os.path.exists(peaks_path):
+            with open(peaks_path) as fh:
+                peak = float(json.load(fh)["hbm_gbs"])
+            peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        achieved = kb / (kern_ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (fp64 reductions)",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "m": m, "n": n, "nnz": len(v), "k": k,
+                       "values": "fp32", "l2": "flushed before every step (512 MiB write)",
+                       "timing": "per-step CUDA events, CUDA-graph replay, max over ranks",
+                       "parallelism": f"{world} row/column shards of one instance "
+                                      "(mfg_sweep_sharded; no data-path collective)",
+                       "rank0_shard": {"rows": r1 - r0, "cols": c1 - c0, "nnz_rows": nnz_r,
+                                       "nnz_cols": nnz_c}},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int((m + n) * k * 4),
+                    "d2h_bytes_per_step": int(24 + (plan.RH.numel() + plan.RtW.numel()) * 4)},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_sweep_g8f on rank 0's shards",
+                         "bytes_per_launch": kb, "avg_launch_us": kern_ms * 1e3,
+                         "peak_source": peak_src},
+            "cpu_baseline": None,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

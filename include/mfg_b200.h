@@ -125,6 +125,22 @@ int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src,
  * with concurrent calls; the sweep leaves its counters zeroed.           */
 size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);
 
+/* The sweep of one rank's shards: rows_csr is the CSR of
+ * the rank's row block R_p (local row ids, global column ids), cols_csc the
+ * CSC of its column block C_p (local column ids, global row ids). W_rows /
+ * H_cols point at the rows R_p of W / C_p of H (the self rows), W_full /
+ * H_full at the replicas the passes gather from. Outputs: R over the row
+ * shard, the rows R_p of R.H and C_p of R^T.W -- final, with no exchange --
+ * and sums = [sum r^2 over the row shard, ||W_rows||^2, ||H_cols||^2], whose
+ * rank-ordered sums are the full sweep's. Same kernels and preconditions as
+ * mfg_sweep; mfg_sweep_workspace(rows_csr, cols_csc, k) sizes the workspace. */
+int mfg_sweep_sharded(int dtype, int compute_f64, const mfg_layout* rows_csr,
+                      const mfg_layout* cols_csc, int k, const void* vals_rows,
+                      const void* vals_cols, const void* W_rows, const void* W_full,
+                      int ldw, const void* H_cols, const void* H_full, int ldh,
+                      void* R, void* RH, void* RtW, double out_scale, double* sums,
+                      void* workspace, size_t ws_bytes, void* stream);
+
 /* mfg_sweep from HOST factors, as a host caller of the reference's sweep
  * (residual_on_omega + loss_quad + res.csr @ H + res.csr_t @ W,
  * mfg/data.py:272-293, mfg/operators.py:108,117) holds them: enqueues on

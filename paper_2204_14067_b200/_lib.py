@@ -105,6 +105,8 @@ _SIGS = {
     "mfg_sweep_workspace": (_SZ, [_LP, _LP, _INT]),
     "mfg_sweep": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _INT, _P, _INT, _P, _P, _P, _D,
                          _P, _P, _SZ, _P]),
+    "mfg_sweep_sharded": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _P, _INT, _P, _P, _INT, _P,
+                                 _P, _P, _D, _P, _P, _SZ, _P]),
     "mfg_sweep_host": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _P, _P, _INT, _P, _INT, _P,
                               _P, _P, _D, _P, _SZ, _P]),
     "mfg_staged_block_rows": (_INT, [_INT]),

@@ -113,6 +113,22 @@ extern "C" int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr, cons
                         RH, RtW, out_scale, sums, workspace, ws_bytes, (cudaStream_t)stream);
 }
 
+extern "C" int mfg_sweep_sharded(int dtype, int compute_f64, const mfg_layout* rows_csr,
+                                 const mfg_layout* cols_csc, int k, const void* vals_rows,
+                                 const void* vals_cols, const void* W_rows, const void* W_full,
+                                 int ldw, const void* H_cols, const void* H_full, int ldh, void* R,
+                                 void* RH, void* RtW, double out_scale, double* sums,
+                                 void* workspace, size_t ws_bytes, void* stream) {
+  MFG_REQUIRE(rows_csr && cols_csc, "null layout");
+  MFG_REQUIRE(k >= 1, "k must be >= 1");
+  MFG_REQUIRE(W_rows && W_full && H_cols && H_full, "null factor");
+  MFG_REQUIRE(rows_csr->ncols >= cols_csc->nrows && cols_csc->ncols >= rows_csr->nrows,
+              "shard layouts do not fit the factor replicas");
+  return sweep_dispatch(dtype, compute_f64, rows_csr, cols_csc, k, vals_rows, vals_cols, W_rows,
+                        ldw, H_cols, ldh, R, RH, RtW, out_scale, sums, workspace, ws_bytes,
+                        (cudaStream_t)stream, W_full, H_full);
+}
+
 extern "C" int mfg_sweep_host(int dtype, int compute_f64, const mfg_layout* csr,
                               const mfg_layout* csc, int k, const void* vals_csr,
                               const void* vals_csc, const void* W_host, const void* H_host,

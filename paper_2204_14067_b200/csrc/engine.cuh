@@ -11,7 +11,8 @@ size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);
 int sweep_dispatch(int dtype, int compute_f64, const mfg_layout* csr, const mfg_layout* csc,
                    int k, const void* vals_csr, const void* vals_csc, const void* W, int ldw,
                    const void* H, int ldh, void* R, void* RH, void* RtW, double out_scale,
-                   double* sums, void* ws, size_t wsb, cudaStream_t stream);
+                   double* sums, void* ws, size_t wsb, cudaStream_t stream,
+                   const void* Wg = nullptr, const void* Hg = nullptr);
 
 size_t sddmm_workspace(const mfg_layout* lay, int k);
 int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,

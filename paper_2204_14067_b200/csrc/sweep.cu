@@ -1489,10 +1489,16 @@ int launch_main(const Pass<TS, TC>& P0, const Pass<TS, TC>& P1, int n0, int n1, 
 }
 
 template <typename TS, typename TC>
+// W / H: the self rows of the CSR / CSC pass (and the rows the norms cover);
+// Wg / Hg: the factors the CSC / CSR pass gathers from. One Omega: Wg = W,
+// Hg = H. A rank's shards (mfg_sweep_sharded): W = its row block of W,
+// H = its column block of H, Wg / Hg = the full replicas.
 int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* vals_csr,
              const void* vals_csc, const void* W, int ldw, const void* H, int ldh, void* R,
              void* RH, void* RtW, double out_scale, double* sums, void* ws, size_t wsb,
-             cudaStream_t stream) {
+             cudaStream_t stream, const void* Wg = nullptr, const void* Hg = nullptr) {
+  if (!Wg) Wg = W;
+  if (!Hg) Hg = H;
   Carver c(ws, wsb);
   // persistent, zero-at-rest state first (fixed offsets for every path)
   int32_t* cnt0 = c.take<int32_t>((size_t)csr->nrows + 1);
@@ -1514,10 +1520,10 @@ int do_sweep(const mfg_layout* csr, const mfg_layout* csc, int k, const void* va
   if (!setup_pass(P1, c, csc, k, acc1, false, grouped ? kpg : 0)) goto small;
   {
     P0.vals = (const TS*)vals_csr; P0.G = nullptr; P0.self = (const TS*)W; P0.lds = ldw;
-    P0.scale = nullptr; P0.other = (const TS*)H; P0.ldo = ldh; P0.R = (TS*)R; P0.r_mult = 1.0;
+    P0.scale = nullptr; P0.other = (const TS*)Hg; P0.ldo = ldh; P0.R = (TS*)R; P0.r_mult = 1.0;
     P0.out = (TS*)RH; P0.ldout = k; P0.out_scale = out_scale; P0.want_sq = 1;
     P1.vals = (const TS*)vals_csc; P1.G = nullptr; P1.self = (const TS*)H; P1.lds = ldh;
-    P1.scale = nullptr; P1.other = (const TS*)W; P1.ldo = ldw; P1.R = nullptr; P1.r_mult = 1.0;
+    P1.scale = nullptr; P1.other = (const TS*)Wg; P1.ldo = ldw; P1.R = nullptr; P1.r_mult = 1.0;
     P1.out = (TS*)RtW; P1.ldout = k; P1.out_scale = out_scale; P1.want_sq = 0;
     SumJob J{};
     {
@@ -1644,15 +1650,16 @@ size_t sddmm_workspace(const mfg_layout* lay, int k) {
 int sweep_dispatch(int dtype, int compute_f64, const mfg_layout* csr, const mfg_layout* csc,
                    int k, const void* vals_csr, const void* vals_csc, const void* W, int ldw,
                    const void* H, int ldh, void* R, void* RH, void* RtW, double out_scale,
-                   double* sums, void* ws, size_t wsb, cudaStream_t stream) {
+                   double* sums, void* ws, size_t wsb, cudaStream_t stream, const void* Wg,
+                   const void* Hg) {
   if (dtype == MFG_F64)
     return do_sweep<double, double>(csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R, RH, RtW,
-                                     out_scale, sums, ws, wsb, stream);
+                                     out_scale, sums, ws, wsb, stream, Wg, Hg);
   if (compute_f64)
     return do_sweep<float, double>(csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R, RH, RtW,
-                                    out_scale, sums, ws, wsb, stream);
+                                    out_scale, sums, ws, wsb, stream, Wg, Hg);
   return do_sweep<float, float>(csr, csc, k, vals_csr, vals_csc, W, ldw, H, ldh, R, RH, RtW,
-                                 out_scale, sums, ws, wsb, stream);
+                                 out_scale, sums, ws, wsb, stream, Wg, Hg);
 }
 
 int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,

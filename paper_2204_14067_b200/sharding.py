@@ -228,3 +228,61 @@ class DeviceOps:
 
         out = torch.zeros((obs.m, block_full.shape[1]), dtype=torch.float64, device=block_full.device)
         return spmm(SparseResidual(obs.m, obs.n, obs, vals), block_full.double(), False, 1.0, 0.0, out)
+
+
+class ShardSweepPlan:
+    """One rank's part of the Omega sweep with the grouped kernel
+    (``mfg_sweep_sharded``): R over the row shard, the rows R_p of R.H, the
+    rows C_p of R^T.W (final: no exchange on the data path) and the local
+    fp64 sums [sum r^2 over the row shard, ||W_{R_p}||^2, ||H_{C_p}||^2].
+
+    ``obs_rows`` / ``obs_cols`` are the ObservationSets of the rank's row
+    shard (local rows x n) and transposed column shard (local columns x m),
+    as ``DeviceOps.prepare`` builds them from a ``Shard``. Factors passed to
+    ``run`` are the full replicas in the grouped kernel's layout (``ld``)."""
+
+    def __init__(self, shard: Shard, obs_rows, obs_cols, k: int, *, want_r: bool = True,
+                 out_scale: float = 1.0):
+        from . import _lib
+        from .mfsolver import grouped_ld
+
+        self.s, self.k = shard, int(k)
+        self.obs_r, self.obs_c = obs_rows, obs_cols
+        dt = obs_rows.dtype
+        if obs_cols.dtype != dt:
+            raise ValueError("row and column shards must share a dtype")
+        self.dt = dt
+        dev = obs_rows.dev.device
+        self.ld = grouped_ld(self.k, dt) or self.k
+        self.out_scale = float(out_scale)
+        r0, r1 = shard.row_block
+        c0, c1 = shard.col_block
+        self.R = torch.empty(obs_rows.size, dtype=dt, device=dev) if want_r else None
+        self.RH = torch.zeros((r1 - r0, self.k), dtype=dt, device=dev)
+        self.RtW = torch.zeros((c1 - c0, self.k), dtype=dt, device=dev)
+        self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        lib = _lib.lib()
+        self.wsb = lib.mfg_sweep_workspace(obs_rows.dev.csr.ref, obs_cols.dev.csr.ref, self.k)
+        self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev)
+
+    def pad(self, f: torch.Tensor) -> torch.Tensor:
+        if self.ld == self.k:
+            return f.to(self.dt).contiguous()
+        out = torch.zeros((f.shape[0], self.ld), dtype=self.dt, device=f.device)
+        out[:, : f.shape[1]] = f
+        return out
+
+    def run(self, w_full: torch.Tensor, h_full: torch.Tensor) -> None:
+        from . import _lib
+
+        r0, _ = self.s.row_block
+        c0, _ = self.s.col_block
+        lib = _lib.lib()
+        es = w_full.element_size()
+        _lib.check(lib.mfg_sweep_sharded(
+            _lib.dtype_code(self.dt), 0, self.obs_r.dev.csr.ref, self.obs_c.dev.csr.ref, self.k,
+            self.obs_r.dev.vals.data_ptr(), self.obs_c.dev.vals.data_ptr(),
+            w_full.data_ptr() + r0 * self.ld * es, w_full.data_ptr(), self.ld,
+            h_full.data_ptr() + c0 * self.ld * es, h_full.data_ptr(), self.ld,
+            _lib.ptr(self.R), self.RH.data_ptr(), self.RtW.data_ptr(), self.out_scale,
+            self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, _lib.stream_ptr()), "sharded sweep")

@@ -251,3 +251,47 @@ def test_sharded_lifting_one_rank_on_gpu_matches_product():
     z = _dense_z()
     ev = np.sort(np.linalg.eigvalsh(z @ z.T))[::-1][:LIFT_K]
     np.testing.assert_allclose(got["eigvals"], ev, rtol=1e-8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 3])
+def test_shard_sweep_plans_reassemble_the_full_sweep(world):
+    """mfg_sweep_sharded on every rank's shards (run one after another on one
+    GPU): R, R.H and R^T.W blocks reassemble the single-GPU grouped sweep,
+    and the rank-ordered sums of the local sums are the full sums."""
+    from paper_2204_14067_b200.data import ObservationSet
+    from paper_2204_14067_b200.mfsolver import SweepPlan
+    m, n, r, c, v = synth.generate("c2", scale=0.2, seed=4)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    k = 20
+    w, h = synth.sweep_factors(m, n, k, seed=6, dtype=np.float32)
+    full = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
+    ref = SweepPlan(full, k)
+    W, H = ref.pad(torch.as_tensor(w).cuda()), ref.pad(torch.as_tensor(h).cuda())
+    ref.run(W, H)
+    ops = sharding.DeviceOps(torch.float32)
+    Rs, RHs, RtWs, sums = [], [None] * world, [None] * world, np.zeros(3)
+    for rank in range(world):
+        s = sharding.make_shard(m, n, r, c, v, rank, world)
+        r0, r1 = s.row_block
+        c0, c1 = s.col_block
+        po = ops.prepare(r1 - r0, n, s.r_rows, s.r_cols, s.r_vals)
+        pc = ops.prepare(c1 - c0, m, s.c_rows, s.c_cols, s.c_vals)
+        plan = sharding.ShardSweepPlan(s, po, pc, k)
+        assert plan.ld == ref.ld
+        plan.run(W, H)
+        torch.cuda.synchronize()
+        Rs.append(plan.R.clone())
+        RHs[rank], RtWs[rank] = plan.RH.clone(), plan.RtW.clone()
+        sums += plan.sums.cpu().numpy()
+    # R: per-entry dots, same arithmetic -> bitwise; row blocks in CSR order
+    assert torch.equal(torch.cat(Rs), ref.R)
+    tol = lambda x: 2e-5 * (float(x.abs().max()) + 1.0)  # noqa: E731  fp32 accumulation order
+    rh = torch.cat(RHs)
+    rtw = torch.cat(RtWs)
+    assert float((rh - ref.RH).abs().max()) <= tol(ref.RH)
+    assert float((rtw - ref.RtW).abs().max()) <= tol(ref.RtW)
+    full_sums = ref.sums.cpu().numpy()
+    assert sums[0] == pytest.approx(full_sums[0], rel=1e-12)
+    assert sums[1] == pytest.approx(full_sums[1], rel=1e-12)
+    assert sums[2] == pytest.approx(full_sums[2], rel=1e-12)
