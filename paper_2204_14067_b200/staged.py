@@ -216,6 +216,8 @@ class StagedPlan:
         src = obs if isinstance(obs, StagedInput) else StagedInput.of(obs)
         if src.vals.dtype != torch.float32:
             raise ValueError("the staged sweep runs on fp32 storage")
+        if src.nnz == 0:
+            raise ValueError("the staged sweep needs a nonempty Omega (use mfg_sweep)")
         smax = block_rows(k)
         if smax <= 0:
             raise ValueError(f"the staged sweep supports 1 <= k <= 64 (got {k})")

@@ -128,6 +128,11 @@ def test_plan_rejects_bad_args():
         ST.StagedPlan(src, 65)
     with pytest.raises(ValueError):
         ST.StagedPlan(src, 8, S=10 ** 6)
+    empty = ST.StagedInput(3, 4, *(torch.zeros(0, dtype=torch.int32),) * 2,
+                           torch.zeros(0, dtype=torch.float32),
+                           *(torch.zeros(0, dtype=torch.int32),) * 2, torch.zeros(0, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        ST.StagedPlan(empty, 8)
 
 
 # --------------------------------------------------------------------- GPU
