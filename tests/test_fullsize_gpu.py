@@ -97,3 +97,53 @@ def test_full_size_sweep_properties(wl):
     torch.cuda.synchronize()
     assert torch.equal(R0, plan.R) and torch.equal(RH0, plan.RH) and torch.equal(RtW0, plan.RtW)
     assert torch.equal(s0, plan.sums)
+
+
+@pytest.mark.parametrize("wl", ["c3"])
+def test_full_size_spmm_and_bcd_properties(wl):
+    """The lifting step's SpMMs and the BCD half-sweep at full size:
+    <G V, U> = <V, G^T U> = sum_e g_e (U_i . V_j) (CSR SpMM, CSC SpMM and
+    SDDMM agree; fp64, 1e-10 rel), and every sampled row of a BCD half-sweep
+    solves its normal equations (lam I + 2 sum_j h_j h_j^T) w_i =
+    2 sum_j a_ij h_j (mfg/mfsolver.py:53-75) to 1e-9 relative."""
+    from paper_2204_14067_b200 import synth
+    from paper_2204_14067_b200.data import ObservationSet, SparseResidual, sddmm
+    from paper_2204_14067_b200.mfsolver import _half_sweep
+    from paper_2204_14067_b200.operators import spmm
+
+    m, n, r, c, v = synth.generate(wl, seed=0)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    p = 48
+    g = torch.randn(obs.size, dtype=torch.float64, device="cuda", generator=gen)
+    G = SparseResidual(m, n, obs, g)
+    V = torch.randn((n, p), dtype=torch.float64, device="cuda", generator=gen)
+    U = torch.randn((m, p), dtype=torch.float64, device="cuda", generator=gen)
+    GV = spmm(G, V, False, 1.0, 0.0, torch.zeros((m, p), dtype=torch.float64, device="cuda"))
+    GtU = spmm(G, U, True, 1.0, 0.0, torch.zeros((n, p), dtype=torch.float64, device="cuda"))
+    lhs = float((GV * U).sum())
+    rhs = float((GtU * V).sum())
+    _, sums = sddmm(obs, U, V, a=False, g=g, want_out=False, dtype=torch.float64)
+    assert lhs == pytest.approx(rhs, rel=1e-10)
+    assert lhs == pytest.approx(float(sums[2]), rel=1e-10)
+    # BCD half-sweep optimality on sampled rows (fp64 storage: the solve is
+    # fp64 in both modes, fp32 mode would only add the output rounding)
+    k = 30
+    lam = 7.0
+    obs = obs.with_dtype(torch.float64)
+    Hf = 0.3 * torch.randn((n, k), dtype=torch.float64, device="cuda", generator=gen)
+    Wn = _half_sweep(obs, False, Hf, lam).double()
+    d = obs.dev
+    ptr = d.csr.ptr.long()
+    cols = d.csr.idx[: obs.size].long()
+    A = d.vals64[: obs.size]
+    H64 = Hf
+    rng = np.random.default_rng(11)
+    for i in rng.integers(0, m, 24):
+        lo, hi = int(ptr[i]), int(ptr[i + 1])
+        Hi = H64[cols[lo:hi]]
+        normal = lam * torch.eye(k, dtype=torch.float64, device="cuda") + 2.0 * Hi.T @ Hi
+        rhs_i = 2.0 * Hi.T @ A[lo:hi]
+        res = normal @ Wn[i] - rhs_i
+        assert float(res.abs().max()) <= 1e-9 * (float(rhs_i.abs().max()) + lam)
