@@ -133,6 +133,8 @@ def _tsqr(comm: ShardComm, b_loc: torch.Tensor):
     p = b_loc.shape[1]
     q_l, r_l = torch.linalg.qr(b_loc, mode="reduced")     # r_l: min(m_p, p) x p
     rows = r_l.shape[0]
+    if comm.world == 1 and rows == p:
+        return q_l, r_l                                     # one block: its QR is the TSQR
     r_pad = torch.zeros((p, p), dtype=b_loc.dtype, device=b_loc.device)
     r_pad[:rows] = r_l
     stack = torch.cat(comm.all_gather_list(r_pad), dim=0)   # (world * p) x p
@@ -161,7 +163,8 @@ def _cholqr2(comm: ShardComm, b_loc: torch.Tensor, scale: float, tol: float):
     return torch.linalg.solve_triangular(r2, q1, upper=True, left=False)
 
 
-def orthonormalize(comm: ShardComm, b_loc: torch.Tensor, m: int, tol: float = ORTH_TOL):
+def orthonormalize(comm: ShardComm, b_loc: torch.Tensor, m: int, tol: float = ORTH_TOL,
+                   fast: list | None = None):
     """Sharded mfg/kernels.py:76-105: orthonormal basis of range(B) (this
     rank's rows of the m x p block) and its rank, screening |R_jj| <= tol *
     ||B||_F on the R of a TSQR and repeating until stable; CholeskyQR2 fast
@@ -172,10 +175,15 @@ def orthonormalize(comm: ShardComm, b_loc: torch.Tensor, m: int, tol: float = OR
     scale = _frob(comm, b_loc)
     if scale == 0.0:
         return b_loc.new_zeros((m_loc, 0)), 0
-    if 8 <= p <= m:
+    # ``fast``: a caller-held switch for the CholeskyQR2 path, cleared by its
+    # first failure (as kernels.orthonormalize: the LM-Krylov candidate
+    # blocks stay ill conditioned once they fail)
+    if 8 <= p <= m and (fast is None or fast[0]):
         q = _cholqr2(comm, b_loc, scale, tol)
         if q is not None:
             return q, p
+        if fast is not None:
+            fast[0] = False
     cols = b_loc
     while True:
         q, r = _tsqr(comm, cols)
@@ -256,10 +264,11 @@ def lmkrylov_topk(op: ShardedOperator, r0_loc: torch.Tensor, cfg: EigConfig) -> 
     basis, w, res = u, np.zeros(k), np.full(k, np.inf)
     converged = False
     it = 0
+    fast_cand, fast_comp = [True], [True]   # CholeskyQR2 fast path per call site
     for it in range(1, cfg.max_iters + 1):
         p_blk = op.apply_gram(u)
         cand = p_blk if cfg.memory == 0 else torch.cat([p_blk, u] + hist, dim=1)
-        q, rank = orthonormalize(comm, cand, m)
+        q, rank = orthonormalize(comm, cand, m, fast=fast_cand)
         if rank < k:
             q = _complete_basis(comm, q, k, op.s.row_block[0], m)
         ritz_vecs, w_all, _, res_all = _ritz(op, q)
@@ -272,7 +281,7 @@ def lmkrylov_topk(op: ShardedOperator, r0_loc: torch.Tensor, cfg: EigConfig) -> 
         stalled = not done and rmax <= _FLOOR * max(w[0], 1e-300)
         if cfg.memory >= 2 and not (done or stalled):
             comp = u - basis @ comm.sum_ordered(basis.T @ u)
-            cq, crank = orthonormalize(comm, comp, m)
+            cq, crank = orthonormalize(comm, comp, m, fast=fast_comp)
             if crank:
                 hist = [cq] + hist
             hist = hist[: cfg.memory - 1]
