@@ -153,3 +153,23 @@ def test_sharded_driver_on_gpu_matches_product_solver(name):
     assert [r.rank for r in trace.records] == tr["rank"] == [r.rank for r in trace_p.records]
     assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-8
     assert np.max(np.abs(got - prod) / np.abs(prod)) <= 1e-8
+
+
+@pytest.mark.gpu
+def test_sharded_driver_fp32_mode_tracks_reference():
+    """fp32 storage of Omega values and MF factors (lifting step and every
+    reduction in fp64), one rank on the GPU: the objective stays within 1e-4
+    relative of the fp64 reference trace and the final rank agrees (the
+    north_star's fp32-mode bar)."""
+    tr = _golden()["mfg_est_crit4"]
+    rows, cols, vals = np.array(tr["rows"]), np.array(tr["cols"]), np.array(tr["vals"])
+    shard = sharding.make_shard(tr["m"], tr["n"], rows, cols, vals, 0, 1)
+    comm = sl.ShardComm()
+    mf = sharding.ShardedMF(shard, sharding.DeviceOps(torch.float32), comm, torch.device("cuda", 0))
+    x, (w, h), trace = ss.solve_mf_global_sharded(mf, comm, _cfg(tr), dtype=torch.float32)
+    assert w.dtype == torch.float32 and h.dtype == torch.float32
+    got = np.array([r.obj for r in trace.records])
+    ref = np.array(tr["obj"])
+    n = min(len(got), len(ref))
+    assert np.max(np.abs(got[:n] - ref[:n]) / np.abs(ref[:n])) <= 1e-4
+    assert trace.records[-1].rank == tr["rank"][-1]
