@@ -24,7 +24,7 @@ template <typename TS>
 __global__ void __launch_bounds__(kNT)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
-      int* __restrict__ bad) {
+      int* __restrict__ bad, int min_d) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int kp = k + 1;                         // padded leading dimension
@@ -36,6 +36,7 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   const int nt4 = (k + 3) / 4;                  // 4x4 tiles per dim
   for (int i = blockIdx.x; i < lay.nrows; i += gridDim.x) {
     const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
+    if (e1 - e0 < min_d) continue;   // done by the packed/dual kernel (row-uniform)
     for (int x = tid; x < k * k; x += kNT) G[x] = 0.0;
     for (int x = tid; x < k; x += kNT) bvec[x] = 0.0;
     __syncthreads();
@@ -162,6 +163,7 @@ k_bcd_packed(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __res
     }
     const bool dual = d < k;
     const int sdim = dual ? d : k;
+    if (sdim > smax) continue;   // system larger than the shared-memory budget: global kernel
     const int npk = sdim * (sdim + 1) / 2;
     for (int x = tid; x < npk; x += kNT) L[x] = 0.0;
     for (int x = tid; x < sdim; x += kNT) vec[x] = 0.0;
@@ -334,6 +336,12 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
   const int grid = global ? 2 * kNumSMs : grid_for_rows(lay->nrows);
   Carver c(ws, wsb);
   int* bad = c.take<int>(1);
+  // k beyond the on-chip primal: rows with few entries still fit on chip as
+  // d x d dual systems (d <= smax); only the heavier rows take the global
+  // k x k path (its Gram and Cholesky live in global scratch)
+  int smax = 0;
+  if (global)
+    while (smax + 1 <= k && smem_packed(k, smax + 1) <= 220 * 1024) ++smax;
   double* gs = global ? c.take<double>((size_t)grid * k * k) : nullptr;
   MFG_REQUIRE(c.ok, "bcd workspace too small");
   const size_t smem = smem_bytes(k, global);
@@ -341,8 +349,17 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
   MFG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+  if (smax >= 1) {
+    const size_t psm = smem_packed(k, smax);
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd_packed<TS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+    k_bcd_packed<TS><<<grid_for_rows(lay->nrows), kNT, psm, stream>>>(
+        *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, smax, bad);
+    MFG_LAUNCH_CHECK();
+  }
   k_bcd<TS><<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
-                                         (TS*)out, ldout, gs, global ? 1 : 0, bad);
+                                         (TS*)out, ldout, gs, global ? 1 : 0, bad,
+                                         smax >= 1 ? smax + 1 : 0);
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }
