@@ -19,6 +19,7 @@ namespace {
 constexpr int kNT = 128;
 constexpr int kC = 16;         // entries staged per chunk
 constexpr int kSmemMaxK = 128; // Gram in shared memory up to this k
+constexpr int kNB = 32;        // panel width of the blocked Cholesky (global path)
 
 template <typename TS>
 __global__ void __launch_bounds__(kNT)
@@ -28,9 +29,14 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int kp = k + 1;                         // padded leading dimension
-  double* stage = sm;                           // [kC][kp]
-  double* sa = stage + kC * kp;                 // [kC]
-  double* bvec = sa + kC;                       // [k]
+  // global path: the Cholesky panel [kNB][k] reuses the staging area, and
+  // the Gram stages as many entries per chunk as that area holds (fewer
+  // read-modify-write passes over the global Gram)
+  const int region = use_global && kNB * k > kC * kp + kC ? kNB * k : kC * kp + kC;
+  const int kc = use_global ? max(kC, min(64, region / (kp + 1))) : kC;  // entries per chunk
+  double* stage = sm;                           // [kc][kp]
+  double* sa = stage + kc * kp;                 // [kc]
+  double* bvec = sm + region;                   // [k]
   double* yvec = bvec + k;                      // [k]
   double* G = use_global ? gscratch + (size_t)blockIdx.x * k * k : yvec + k;  // [k][k]
   const int nt4 = (k + 3) / 4;                  // 4x4 tiles per dim
@@ -40,15 +46,15 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
     for (int x = tid; x < k * k; x += kNT) G[x] = 0.0;
     for (int x = tid; x < k; x += kNT) bvec[x] = 0.0;
     __syncthreads();
-    for (int c0 = e0; c0 < e1; c0 += kC) {
-      const int cn = min(kC, e1 - c0);
-      for (int x = tid; x < kC * k; x += kNT) {
+    for (int c0 = e0; c0 < e1; c0 += kc) {
+      const int cn = min(kc, e1 - c0);
+      for (int x = tid; x < kc * k; x += kNT) {
         const int c = x / k, d = x - c * k;
         double v = 0.0;
         if (c < cn) v = (double)other[(int64_t)lay.idx[c0 + c] * ldo + d];
         stage[c * kp + d] = v;
       }
-      if (tid < kC) sa[tid] = tid < cn ? (double)vals[c0 + tid] : 0.0;
+      for (int c = tid; c < kc; c += kNT) sa[c] = c < cn ? (double)vals[c0 + c] : 0.0;
       __syncthreads();
       // Gram tiles (upper triangle incl. diagonal)
       for (int t = tid; t < nt4 * nt4; t += kNT) {
@@ -95,22 +101,95 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
     for (int x = tid; x < k; x += kNT) bvec[x] *= 2.0;
     __syncthreads();
     // Cholesky N = U^T U, U upper, in place (right-looking)
-    for (int j = 0; j < k; ++j) {
-      if (tid == 0) {
-        const double djj = G[j * k + j];
-        if (!(djj > 0.0)) atomicOr(bad, 1);
-        G[j * k + j] = sqrt(djj);
+    if (!use_global) {
+      for (int j = 0; j < k; ++j) {
+        if (tid == 0) {
+          const double djj = G[j * k + j];
+          if (!(djj > 0.0)) atomicOr(bad, 1);
+          G[j * k + j] = sqrt(djj);
+        }
+        __syncthreads();
+        const double ujj = G[j * k + j];
+        for (int q = j + 1 + tid; q < k; q += kNT) G[j * k + q] /= ujj;
+        __syncthreads();
+        const int rem = k - j - 1;
+        for (int x = tid; x < rem * rem; x += kNT) {
+          const int p = j + 1 + x / rem, q = j + 1 + x % rem;
+          if (q >= p) G[p * k + q] -= G[j * k + p] * G[j * k + q];
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      const double ujj = G[j * k + j];
-      for (int q = j + 1 + tid; q < k; q += kNT) G[j * k + q] /= ujj;
-      __syncthreads();
-      const int rem = k - j - 1;
-      for (int x = tid; x < rem * rem; x += kNT) {
-        const int p = j + 1 + x / rem, q = j + 1 + x % rem;
-        if (q >= p) G[p * k + q] -= G[j * k + p] * G[j * k + q];
+    } else {
+      // Blocked right-looking Cholesky on the global scratch: a panel of
+      // kNB rows of U is factored in shared memory, then the trailing
+      // matrix takes one rank-kNB update (4x4 register tiles), so each
+      // trailing entry is read and written once per panel instead of once
+      // per column.
+      double* P = stage;  // [kNB][k]
+      for (int jb = 0; jb < k; jb += kNB) {
+        const int w = min(kNB, k - jb);
+        const int wc = k - jb;
+        for (int x = tid; x < w * wc; x += kNT) {
+          const int r = x / wc, c = jb + x - r * wc;
+          P[r * k + c] = G[(int64_t)(jb + r) * k + c];
+        }
+        __syncthreads();
+        for (int j = 0; j < w; ++j) {
+          const int jj = jb + j;
+          if (tid == 0) {
+            const double djj = P[j * k + jj];
+            if (!(djj > 0.0)) atomicOr(bad, 1);
+            P[j * k + jj] = sqrt(djj);
+          }
+          __syncthreads();
+          const double ujj = P[j * k + jj];
+          for (int q = jj + 1 + tid; q < k; q += kNT) P[j * k + q] /= ujj;
+          __syncthreads();
+          const int nr = w - j - 1;
+          for (int x = tid; x < nr * wc; x += kNT) {
+            const int r = j + 1 + x / wc, q = jb + x % wc;
+            if (q >= jb + r) P[r * k + q] -= P[j * k + jb + r] * P[j * k + q];
+          }
+          __syncthreads();
+        }
+        for (int x = tid; x < w * wc; x += kNT) {
+          const int r = x / wc, c = jb + x - r * wc;
+          if (c >= jb + r) G[(int64_t)(jb + r) * k + c] = P[r * k + c];
+        }
+        // trailing update G[p][q] -= sum_r P[r][p] P[r][q], p, q >= jb + w
+        const int t0 = jb + w, n = k - t0;
+        const int nt = (n + 3) / 4;
+        for (int t = tid; t < nt * nt; t += kNT) {
+          const int tp = t / nt, tq = t - tp * nt;
+          if (tq < tp) continue;
+          double acc[4][4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+          for (int r = 0; r < w; ++r) {
+            double xp[4], xq[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const int p = t0 + tp * 4 + a, q = t0 + tq * 4 + a;
+              xp[a] = p < k ? P[r * k + p] : 0.0;
+              xq[a] = q < k ? P[r * k + q] : 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] = fma(xp[a], xq[b], acc[a][b]);
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int p = t0 + tp * 4 + a, q = t0 + tq * 4 + b;
+              if (p < k && q < k && q >= p) G[(int64_t)p * k + q] -= acc[a][b];
+            }
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
     // U^T y = rhs
     for (int j = 0; j < k; ++j) {
@@ -303,7 +382,8 @@ size_t smem_packed(int k, int smax) {
 
 size_t smem_bytes(int k, bool global) {
   const int kp = k + 1;
-  size_t n = (size_t)kC * kp + kC + 2 * (size_t)k;
+  const size_t region = (size_t)kC * kp + kC;
+  size_t n = (global && (size_t)kNB * k > region ? (size_t)kNB * k : region) + 2 * (size_t)k;
   if (!global) n += (size_t)k * k;
   return n * sizeof(double);
 }

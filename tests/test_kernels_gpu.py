@@ -269,7 +269,7 @@ def test_grouped_sweep_vs_oracle(k, dtype, layout):
     assert sums_h.numpy()[0] == pytest.approx(sq2, rel=tol * 10)
 
 
-@pytest.mark.parametrize("k", [130, 150, 200, 260])
+@pytest.mark.parametrize("k", [130, 150, 200, 260, 300])
 def test_bcd_large_k_packed_and_dual(k):
     """k > 128: packed shared-memory Cholesky; rows with fewer entries than k
     take the push-through (dual) d x d solve. Rows here have ~200 entries on
