@@ -7,7 +7,7 @@
 #define CK(x) do { auto e = (x); if (e != 0) { printf("err %d at %s:%d\n", (int)e, __FILE__, __LINE__); exit(1); } } while (0)
 int main() {
   cusolverDnHandle_t h; CK(cusolverDnCreate(&h));
-  for (int n : {256, 512, 1024, 1400}) {
+  for (int n : {288, 576, 1024, 1400}) {
     std::vector<double> A(n * n);
     srand(1);
     for (int i = 0; i < n; ++i) for (int j = 0; j <= i; ++j) { double v = rand() / (double)RAND_MAX - 0.5; A[i * n + j] = A[j * n + i] = v; }
