@@ -21,8 +21,8 @@ constexpr int kC = 16;         // entries staged per chunk
 constexpr int kSmemMaxK = 128; // Gram in shared memory up to this k
 constexpr int kNB = 32;        // panel width of the blocked Cholesky (global path)
 
-template <typename TS>
-__global__ void __launch_bounds__(kNT)
+template <typename TS, int NT = kNT>
+__global__ void __launch_bounds__(NT)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
       int* __restrict__ bad, int min_d) {
@@ -32,7 +32,9 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   // global path: the Cholesky panel [kNB][k] reuses the staging area, and
   // the Gram stages as many entries per chunk as that area holds (fewer
   // read-modify-write passes over the global Gram)
-  const int region = use_global && kNB * k > kC * kp + kC ? kNB * k : kC * kp + kC;
+  const int region0 = use_global && kNB * k > kC * kp + kC ? kNB * k : kC * kp + kC;
+  const int region = use_global && 32 * (64 + 4 * (NT / 16)) > region0 ? 32 * (64 + 4 * (NT / 16))
+                                                                      : region0;
   const int kc = use_global ? max(kC, min(64, region / (kp + 1))) : kC;  // entries per chunk
   double* stage = sm;                           // [kc][kp]
   double* sa = stage + kc * kp;                 // [kc]
@@ -43,62 +45,122 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   for (int i = blockIdx.x; i < lay.nrows; i += gridDim.x) {
     const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
     if (e1 - e0 < min_d) continue;   // done by the packed/dual kernel (row-uniform)
-    for (int x = tid; x < k * k; x += kNT) G[x] = 0.0;
-    for (int x = tid; x < k; x += kNT) bvec[x] = 0.0;
+    if (!use_global)                 // the global path writes every upper entry once
+      for (int x = tid; x < k * k; x += NT) G[x] = 0.0;
+    for (int x = tid; x < k; x += NT) bvec[x] = 0.0;
     __syncthreads();
-    for (int c0 = e0; c0 < e1; c0 += kc) {
-      const int cn = min(kc, e1 - c0);
-      for (int x = tid; x < kc * k; x += kNT) {
-        const int c = x / k, d = x - c * k;
-        double v = 0.0;
-        if (c < cn) v = (double)other[(int64_t)lay.idx[c0 + c] * ldo + d];
-        stage[c * kp + d] = v;
+    if (!use_global) {
+      for (int c0 = e0; c0 < e1; c0 += kc) {
+        const int cn = min(kc, e1 - c0);
+        for (int x = tid; x < kc * k; x += NT) {
+          const int c = x / k, d = x - c * k;
+          double v = 0.0;
+          if (c < cn) v = (double)other[(int64_t)lay.idx[c0 + c] * ldo + d];
+          stage[c * kp + d] = v;
+        }
+        for (int c = tid; c < kc; c += NT) sa[c] = c < cn ? (double)vals[c0 + c] : 0.0;
+        __syncthreads();
+        // Gram tiles (upper triangle incl. diagonal)
+        for (int t = tid; t < nt4 * nt4; t += NT) {
+          const int tp = t / nt4, tq = t - tp * nt4;
+          if (tq < tp) continue;
+          double accv[4][4];
+  #pragma unroll
+          for (int a = 0; a < 4; ++a)
+  #pragma unroll
+            for (int b = 0; b < 4; ++b) accv[a][b] = 0.0;
+          for (int c = 0; c < cn; ++c) {
+            double xp[4], xq[4];
+  #pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              const int p = tp * 4 + a, q = tq * 4 + a;
+              xp[a] = p < k ? stage[c * kp + p] : 0.0;
+              xq[a] = q < k ? stage[c * kp + q] : 0.0;
+            }
+  #pragma unroll
+            for (int a = 0; a < 4; ++a)
+  #pragma unroll
+              for (int b = 0; b < 4; ++b) accv[a][b] = fma(xp[a], xq[b], accv[a][b]);
+          }
+  #pragma unroll
+          for (int a = 0; a < 4; ++a)
+  #pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int p = tp * 4 + a, q = tq * 4 + b;
+              if (p < k && q < k && q >= p) G[p * k + q] += accv[a][b];
+            }
+        }
+        for (int d = tid; d < k; d += NT) {
+          double s = 0.0;
+          for (int c = 0; c < cn; ++c) s = fma(sa[c], stage[c * kp + d], s);
+          bvec[d] += s;
+        }
+        __syncthreads();
       }
-      for (int c = tid; c < kc; c += kNT) sa[c] = c < cn ? (double)vals[c0 + c] : 0.0;
-      __syncthreads();
-      // Gram tiles (upper triangle incl. diagonal)
-      for (int t = tid; t < nt4 * nt4; t += kNT) {
-        const int tp = t / nt4, tq = t - tp * nt4;
-        if (tq < tp) continue;
-        double accv[4][4];
+    } else {
+      // Heavy rows, k beyond shared memory: GEMM-shaped Gram. Each 64 x 32
+      // tile of G (4x4 register tiles, 128 threads) accumulates over all of
+      // the row's entries, streamed through shared memory 32 at a time, and
+      // is written once -- no read-modify-write of the global Gram per chunk.
+      for (int e = e0; e < e1; ++e) {
+        const double a = (double)vals[e];
+        const TS* hrow = other + (int64_t)lay.idx[e] * ldo;
+        for (int d = tid; d < k; d += NT) bvec[d] = fma(a, (double)hrow[d], bvec[d]);
+      }
+      constexpr int TX = NT / 16;          // thread columns; 16 thread rows
+      constexpr int TQ = 4 * TX;           // tile: 64 x TQ
+      double* sP = stage;                 // [32][64]
+      double* sQ = stage + 32 * 64;       // [32][TQ]
+      const int ty = tid / TX, tx = tid % TX;
+      for (int pb = 0; pb < k; pb += 64) {
+        for (int qb = pb; qb < k; qb += TQ) {
+          double acc[4][4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) accv[a][b] = 0.0;
-        for (int c = 0; c < cn; ++c) {
-          double xp[4], xq[4];
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+          for (int c0 = e0; c0 < e1; c0 += 32) {
+            const int cn = min(32, e1 - c0);
+            __syncthreads();   // the previous chunk's reads are done
+            for (int x = tid; x < 32 * (64 + TQ); x += NT) {
+              const int c = x / (64 + TQ), j = x - c * (64 + TQ);
+              double v = 0.0;
+              const int dim = j < 64 ? pb + j : qb + (j - 64);
+              if (c < cn && dim < k) v = (double)other[(int64_t)lay.idx[c0 + c] * ldo + dim];
+              if (j < 64) sP[c * 64 + j] = v;
+              else sQ[c * TQ + (j - 64)] = v;
+            }
+            __syncthreads();
+            for (int c = 0; c < cn; ++c) {
+              double xp[4], xq[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int p = tp * 4 + a, q = tq * 4 + a;
-            xp[a] = p < k ? stage[c * kp + p] : 0.0;
-            xq[a] = q < k ? stage[c * kp + q] : 0.0;
+              for (int a = 0; a < 4; ++a) {
+                xp[a] = sP[c * 64 + ty * 4 + a];
+                xq[a] = sQ[c * TQ + tx * 4 + a];
+              }
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(xp[a], xq[b], acc[a][b]);
+            }
           }
 #pragma unroll
           for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) accv[a][b] = fma(xp[a], xq[b], accv[a][b]);
+            for (int b = 0; b < 4; ++b) {
+              const int pp = pb + ty * 4 + a, qq = qb + tx * 4 + b;
+              if (pp < k && qq < k && qq >= pp) G[(int64_t)pp * k + qq] = acc[a][b];
+            }
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int p = tp * 4 + a, q = tq * 4 + b;
-            if (p < k && q < k && q >= p) G[p * k + q] += accv[a][b];
-          }
-      }
-      for (int d = tid; d < k; d += kNT) {
-        double s = 0.0;
-        for (int c = 0; c < cn; ++c) s = fma(sa[c], stage[c * kp + d], s);
-        bvec[d] += s;
       }
       __syncthreads();
     }
     // N = lam I + 2 G (upper), rhs = 2 b
-    for (int x = tid; x < k * k; x += kNT) {
+    for (int x = tid; x < k * k; x += NT) {
       const int p = x / k, q = x - p * k;
       if (q >= p) G[x] = 2.0 * G[x] + (p == q ? lam : 0.0);
     }
-    for (int x = tid; x < k; x += kNT) bvec[x] *= 2.0;
+    for (int x = tid; x < k; x += NT) bvec[x] *= 2.0;
     __syncthreads();
     // Cholesky N = U^T U, U upper, in place (right-looking)
     if (!use_global) {
@@ -110,10 +172,10 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
         }
         __syncthreads();
         const double ujj = G[j * k + j];
-        for (int q = j + 1 + tid; q < k; q += kNT) G[j * k + q] /= ujj;
+        for (int q = j + 1 + tid; q < k; q += NT) G[j * k + q] /= ujj;
         __syncthreads();
         const int rem = k - j - 1;
-        for (int x = tid; x < rem * rem; x += kNT) {
+        for (int x = tid; x < rem * rem; x += NT) {
           const int p = j + 1 + x / rem, q = j + 1 + x % rem;
           if (q >= p) G[p * k + q] -= G[j * k + p] * G[j * k + q];
         }
@@ -129,7 +191,7 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
       for (int jb = 0; jb < k; jb += kNB) {
         const int w = min(kNB, k - jb);
         const int wc = k - jb;
-        for (int x = tid; x < w * wc; x += kNT) {
+        for (int x = tid; x < w * wc; x += NT) {
           const int r = x / wc, c = jb + x - r * wc;
           P[r * k + c] = G[(int64_t)(jb + r) * k + c];
         }
@@ -143,23 +205,23 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
           }
           __syncthreads();
           const double ujj = P[j * k + jj];
-          for (int q = jj + 1 + tid; q < k; q += kNT) P[j * k + q] /= ujj;
+          for (int q = jj + 1 + tid; q < k; q += NT) P[j * k + q] /= ujj;
           __syncthreads();
           const int nr = w - j - 1;
-          for (int x = tid; x < nr * wc; x += kNT) {
+          for (int x = tid; x < nr * wc; x += NT) {
             const int r = j + 1 + x / wc, q = jb + x % wc;
             if (q >= jb + r) P[r * k + q] -= P[j * k + jb + r] * P[j * k + q];
           }
           __syncthreads();
         }
-        for (int x = tid; x < w * wc; x += kNT) {
+        for (int x = tid; x < w * wc; x += NT) {
           const int r = x / wc, c = jb + x - r * wc;
           if (c >= jb + r) G[(int64_t)(jb + r) * k + c] = P[r * k + c];
         }
         // trailing update G[p][q] -= sum_r P[r][p] P[r][q], p, q >= jb + w
         const int t0 = jb + w, n = k - t0;
         const int nt = (n + 3) / 4;
-        for (int t = tid; t < nt * nt; t += kNT) {
+        for (int t = tid; t < nt * nt; t += NT) {
           const int tp = t / nt, tq = t - tp * nt;
           if (tq < tp) continue;
           double acc[4][4];
@@ -196,7 +258,7 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
       if (tid == 0) yvec[j] = bvec[j] / G[j * k + j];
       __syncthreads();
       const double yj = yvec[j];
-      for (int q = j + 1 + tid; q < k; q += kNT) bvec[q] -= G[j * k + q] * yj;
+      for (int q = j + 1 + tid; q < k; q += NT) bvec[q] -= G[j * k + q] * yj;
       __syncthreads();
     }
     // U w = y  (w stored into bvec)
@@ -204,10 +266,10 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
       if (tid == 0) bvec[j] = yvec[j] / G[j * k + j];
       __syncthreads();
       const double wj = bvec[j];
-      for (int p = tid; p < j; p += kNT) yvec[p] -= G[p * k + j] * wj;
+      for (int p = tid; p < j; p += NT) yvec[p] -= G[p * k + j] * wj;
       __syncthreads();
     }
-    for (int d = tid; d < k; d += kNT) out[(int64_t)i * ldout + d] = (TS)bvec[d];
+    for (int d = tid; d < k; d += NT) out[(int64_t)i * ldout + d] = (TS)bvec[d];
     __syncthreads();
   }
 }
@@ -380,10 +442,17 @@ size_t smem_packed(int k, int smax) {
   return ((size_t)smax * (smax + 1) / 2 + 2 * (size_t)kC * kp + 2 * (size_t)v) * sizeof(double);
 }
 
+constexpr int kNTG = 512;      // threads of the global (heavy-row) path: 16 warps per SM
+
 size_t smem_bytes(int k, bool global) {
   const int kp = k + 1;
-  const size_t region = (size_t)kC * kp + kC;
-  size_t n = (global && (size_t)kNB * k > region ? (size_t)kNB * k : region) + 2 * (size_t)k;
+  size_t region = (size_t)kC * kp + kC;
+  if (global) {
+    if ((size_t)kNB * k > region) region = (size_t)kNB * k;
+    const size_t gt = 32 * (64 + 4 * (kNTG / 16));
+    if (gt > region) region = gt;
+  }
+  size_t n = region + 2 * (size_t)k;
   if (!global) n += (size_t)k * k;
   return n * sizeof(double);
 }
@@ -413,7 +482,7 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
     return MFG_OK;
   }
   const bool global = k > kSmemMaxK;
-  const int grid = global ? 2 * kNumSMs : grid_for_rows(lay->nrows);
+  const int grid = global ? kNumSMs : grid_for_rows(lay->nrows);
   Carver c(ws, wsb);
   int* bad = c.take<int>(1);
   // k beyond the on-chip primal: rows with few entries still fit on chip as
@@ -425,9 +494,12 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
   double* gs = global ? c.take<double>((size_t)grid * k * k) : nullptr;
   MFG_REQUIRE(c.ok, "bcd workspace too small");
   const size_t smem = smem_bytes(k, global);
-  if (smem > 48 * 1024)
+  if (smem > 48 * 1024) {
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNTG>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
   MFG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), stream));
   if (smax >= 1) {
     const size_t psm = smem_packed(k, smax);
@@ -437,9 +509,13 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
         *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, smax, bad);
     MFG_LAUNCH_CHECK();
   }
-  k_bcd<TS><<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
-                                         (TS*)out, ldout, gs, global ? 1 : 0, bad,
-                                         smax >= 1 ? smax + 1 : 0);
+  if (global)
+    k_bcd<TS, kNTG><<<grid, kNTG, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo,
+                                                 lam, (TS*)out, ldout, gs, 1, bad,
+                                                 smax >= 1 ? smax + 1 : 0);
+  else
+    k_bcd<TS><<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
+                                           (TS*)out, ldout, gs, 0, bad, 0);
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }
