@@ -10,6 +10,8 @@
 // into shared memory, and the SPD system is solved in place by Cholesky.
 // Nothing of size (m, k, k) ever exists, so config 5 (n ~ 1e6, k = 64) runs.
 // Arithmetic is fp64 for both storage types.
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "engine.cuh"
 
@@ -21,11 +23,27 @@ constexpr int kC = 16;         // entries staged per chunk
 constexpr int kSmemMaxK = 128; // Gram in shared memory up to this k
 constexpr int kNB = 32;        // panel width of the blocked Cholesky (global path)
 
+// Row scheduling: the rows of a half-sweep cost ~ d_i k^2 and are Zipf-
+// skewed (c2: the heaviest row is 6x the mean per-CTA load of a static
+// round-robin split; ncu showed the busiest SM active 2.7x the average).
+// CTAs therefore take rows from a ticket counter in decreasing-degree order
+// (longest first), so the heavy rows start at once and the light ones fill
+// in behind them. Which CTA solves a row does not change its arithmetic.
+// Double-buffered shared ticket: the barrier of the next take orders this
+// take's reads before the buffer is written again.
+__device__ __forceinline__ int take_row(int* ticket, int* s_t, int& par) {
+  if (threadIdx.x == 0) s_t[par] = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int t = s_t[par];
+  par ^= 1;
+  return t;
+}
+
 template <typename TS, int NT = kNT>
 __global__ void __launch_bounds__(NT)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
-      int* __restrict__ bad, int min_d) {
+      int* __restrict__ bad, int min_d, const int* __restrict__ order, int* __restrict__ ticket) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int kp = k + 1;                         // padded leading dimension
@@ -42,9 +60,14 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   double* yvec = bvec + k;                      // [k]
   double* G = use_global ? gscratch + (size_t)blockIdx.x * k * k : yvec + k;  // [k][k]
   const int nt4 = (k + 3) / 4;                  // 4x4 tiles per dim
-  for (int i = blockIdx.x; i < lay.nrows; i += gridDim.x) {
+  __shared__ int s_t[2];
+  int par = 0;
+  for (;;) {
+    const int t = take_row(ticket, s_t, par);
+    if (t >= lay.nrows) break;
+    const int i = order[t];
     const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
-    if (e1 - e0 < min_d) continue;   // done by the packed/dual kernel (row-uniform)
+    if (e1 - e0 < min_d) break;   // rows in decreasing degree: the rest are the packed/dual kernel's
     if (!use_global)                 // the global path writes every upper entry once
       for (int x = tid; x < k * k; x += NT) G[x] = 0.0;
     for (int x = tid; x < k; x += NT) bvec[x] = 0.0;
@@ -286,7 +309,8 @@ __device__ __forceinline__ int tri(int p, int q) { return p * (p + 1) / 2 + q; }
 template <typename TS>
 __global__ void __launch_bounds__(kNT)
 k_bcd_packed(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other,
-             int ldo, double lam, TS* __restrict__ out, int ldout, int smax, int* __restrict__ bad) {
+             int ldo, double lam, TS* __restrict__ out, int ldout, int smax, int* __restrict__ bad,
+             const int* __restrict__ order, int* __restrict__ ticket) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int kp = k + 1;
@@ -295,7 +319,12 @@ k_bcd_packed(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __res
   double* stB = stA + kC * kp;                        // [kC][kp]
   double* vec = stB + kC * kp;                        // [max(k, smax)] rhs / solution
   double* aux = vec + (k > smax ? k : smax);          // [max(k, smax)]
-  for (int i = blockIdx.x; i < lay.nrows; i += gridDim.x) {
+  __shared__ int s_t[2];
+  int par = 0;
+  for (;;) {
+    const int t = take_row(ticket, s_t, par);
+    if (t >= lay.nrows) break;
+    const int i = order[t];
     const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
     const int d = e1 - e0;
     if (d == 0) {
@@ -464,6 +493,56 @@ int grid_for_rows(int nrows) {
   return g;
 }
 
+__global__ void k_row_degrees(const int32_t* __restrict__ ptr, int n, unsigned* __restrict__ key,
+                              int* __restrict__ row) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    key[i] = (unsigned)(ptr[i + 1] - ptr[i]);
+    row[i] = i;
+  }
+}
+
+size_t sort_temp_bytes(int n) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (unsigned*)nullptr, (unsigned*)nullptr,
+                                            (int*)nullptr, (int*)nullptr, n);
+  return b;
+}
+
+// Scheduling workspace: row order (decreasing degree) and two tickets.
+struct RowSched {
+  int* order = nullptr;
+  int* ticket = nullptr;   // [2], zeroed per call
+};
+
+template <typename C>
+void take_sched(C& c, int n, RowSched* rs, unsigned** kin, unsigned** kout, int* *rin, void** tmp,
+                size_t* tmpb) {
+  *kin = c.template take<unsigned>(n);
+  *kout = c.template take<unsigned>(n);
+  *rin = c.template take<int>(n);
+  rs->order = c.template take<int>(n);
+  rs->ticket = c.template take<int>(2);
+  *tmpb = sort_temp_bytes(n);
+  *tmp = c.template take<char>(*tmpb);
+}
+
+int build_sched(const mfg_layout* lay, Carver& c, RowSched* rs, cudaStream_t stream) {
+  const int n = lay->nrows;
+  unsigned *kin, *kout;
+  int* rin;
+  void* tmp;
+  size_t tmpb;
+  take_sched(c, n, rs, &kin, &kout, &rin, &tmp, &tmpb);
+  MFG_REQUIRE(c.ok, "bcd workspace too small");
+  k_row_degrees<<<(n + 255) / 256, 256, 0, stream>>>(lay->ptr, n, kin, rin);
+  MFG_LAUNCH_CHECK();
+  MFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(tmp, tmpb, kin, kout, rin, rs->order, n,
+                                                           0, 32, stream));
+  MFG_CUDA_CHECK(cudaMemsetAsync(rs->ticket, 0, 2 * sizeof(int), stream));
+  return MFG_OK;
+}
+
 template <typename TS>
 int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, int ldo, double lam,
            void* out, int ldout, void* ws, size_t wsb, cudaStream_t stream) {
@@ -472,12 +551,15 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
     Carver c(ws, wsb);
     int* bad = c.take<int>(1);
     MFG_REQUIRE(c.ok, "bcd workspace too small");
+    RowSched rs;
+    if (int st = build_sched(lay, c, &rs, stream)) return st;
     const size_t smem = smem_packed(k, k);
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd_packed<TS>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MFG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), stream));
     k_bcd_packed<TS><<<grid_for_rows(lay->nrows), kNT, smem, stream>>>(
-        *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, k, bad);
+        *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, k, bad, rs.order,
+        rs.ticket);
     MFG_LAUNCH_CHECK();
     return MFG_OK;
   }
@@ -493,6 +575,8 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
     while (smax + 1 <= k && smem_packed(k, smax + 1) <= 220 * 1024) ++smax;
   double* gs = global ? c.take<double>((size_t)grid * k * k) : nullptr;
   MFG_REQUIRE(c.ok, "bcd workspace too small");
+  RowSched rs;
+  if (int st = build_sched(lay, c, &rs, stream)) return st;
   const size_t smem = smem_bytes(k, global);
   if (smem > 48 * 1024) {
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -506,16 +590,17 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd_packed<TS>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
     k_bcd_packed<TS><<<grid_for_rows(lay->nrows), kNT, psm, stream>>>(
-        *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, smax, bad);
+        *lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, smax, bad, rs.order,
+        rs.ticket);
     MFG_LAUNCH_CHECK();
   }
   if (global)
     k_bcd<TS, kNTG><<<grid, kNTG, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo,
                                                  lam, (TS*)out, ldout, gs, 1, bad,
-                                                 smax >= 1 ? smax + 1 : 0);
+                                                 smax >= 1 ? smax + 1 : 0, rs.order, rs.ticket + 1);
   else
     k_bcd<TS><<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
-                                           (TS*)out, ldout, gs, 0, bad, 0);
+                                           (TS*)out, ldout, gs, 0, bad, 0, rs.order, rs.ticket);
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }
@@ -526,6 +611,12 @@ size_t bcd_workspace(const mfg_layout* lay, int k) {
   Sizer s;
   s.take<int>(1);
   if (k > kSmemMaxK) s.take<double>((size_t)2 * kNumSMs * k * k);
+  RowSched rs;
+  unsigned *kin, *kout;
+  int* rin;
+  void* tmp;
+  size_t tmpb;
+  take_sched(s, lay ? lay->nrows : 0, &rs, &kin, &kout, &rin, &tmp, &tmpb);
   return s.off + 512;
 }
 

@@ -72,7 +72,10 @@ struct Carver {
 struct Sizer {
   size_t off = 0;
   template <typename T>
-  void take(size_t count) { off += align_up(count * sizeof(T)); }
+  T* take(size_t count) {
+    off += align_up(count * sizeof(T));
+    return nullptr;
+  }
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
