@@ -31,6 +31,17 @@ constexpr int kNB = 32;        // panel width of the blocked Cholesky (global pa
 // in behind them. Which CTA solves a row does not change its arithmetic.
 // Double-buffered shared ticket: the barrier of the next take orders this
 // take's reads before the buffer is written again.
+// Heavy rows (d > S) of the shared-memory path are cut into segments of S
+// entries; items[u] = (position in the row order, segment, segments, first
+// item of the row) for u < info[1]; info[0] = number of split rows.
+struct SplitPlan {
+  const int4* items = nullptr;
+  const int* info = nullptr;
+  int* done = nullptr;        // per split row: segments finished (zero at rest)
+  double* part = nullptr;     // per item: packed upper Gram + rhs
+  int S = 0;
+};
+
 __device__ __forceinline__ int take_row(int* ticket, int* s_t, int& par) {
   if (threadIdx.x == 0) s_t[par] = atomicAdd(ticket, 1);
   __syncthreads();
@@ -39,11 +50,14 @@ __device__ __forceinline__ int take_row(int* ticket, int* s_t, int& par) {
   return t;
 }
 
+// 5 CTAs per SM at 128 threads (<= 102 registers): the split-row logic
+// otherwise raises the allocation to 124 registers and costs a CTA per SM
 template <typename TS, int NT = kNT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, NT == kNT ? 5 : 1)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
-      int* __restrict__ bad, int min_d, const int* __restrict__ order, int* __restrict__ ticket) {
+      int* __restrict__ bad, int min_d, const int* __restrict__ order, int* __restrict__ ticket,
+      SplitPlan sp) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x;
   const int kp = k + 1;                         // padded leading dimension
@@ -61,20 +75,34 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   double* G = use_global ? gscratch + (size_t)blockIdx.x * k * k : yvec + k;  // [k][k]
   const int nt4 = (k + 3) / 4;                  // 4x4 tiles per dim
   __shared__ int s_t[2];
+  __shared__ int s_last;
   int par = 0;
+  const int nhr = sp.items ? sp.info[0] : 0;   // split (heavy) rows: a prefix of the order
+  const int nhi = sp.items ? sp.info[1] : 0;   // their segment items, taken first
+  const int pslot = k * (k + 1) / 2 + k;       // packed upper Gram + rhs per segment
   for (;;) {
-    const int t = take_row(ticket, s_t, par);
-    if (t >= lay.nrows) break;
-    const int i = order[t];
+    const int u = take_row(ticket, s_t, par);
+    int i, seg = 0, nseg = 1, ibase = 0, hidx = -1, s0, s1;
+    if (u < nhi) {
+      const int4 it = sp.items[u];   // (position in order, segment, segments, first item)
+      hidx = it.x; seg = it.y; nseg = it.z; ibase = it.w;
+      i = order[hidx];
+    } else {
+      const int t = u - nhi + nhr;
+      if (t >= lay.nrows) break;
+      i = order[t];
+    }
     const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
     if (e1 - e0 < min_d) break;   // rows in decreasing degree: the rest are the packed/dual kernel's
+    s0 = e0 + seg * sp.S;
+    s1 = nseg > 1 ? min(e1, s0 + sp.S) : e1;
     if (!use_global)                 // the global path writes every upper entry once
       for (int x = tid; x < k * k; x += NT) G[x] = 0.0;
     for (int x = tid; x < k; x += NT) bvec[x] = 0.0;
     __syncthreads();
     if (!use_global) {
-      for (int c0 = e0; c0 < e1; c0 += kc) {
-        const int cn = min(kc, e1 - c0);
+      for (int c0 = s0; c0 < s1; c0 += kc) {
+        const int cn = min(kc, s1 - c0);
         for (int x = tid; x < kc * k; x += NT) {
           const int c = x / k, d = x - c * k;
           double v = 0.0;
@@ -118,6 +146,40 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
           for (int c = 0; c < cn; ++c) s = fma(sa[c], stage[c * kp + d], s);
           bvec[d] += s;
         }
+        __syncthreads();
+      }
+      if (nseg > 1) {
+        // Heavy row split into segments: publish this segment's partial Gram
+        // and rhs; the CTA finishing the row's last segment sums all partials
+        // in segment order (fixed, so the result does not depend on which
+        // CTA ran which segment) and solves.
+        double* slot = sp.part + (size_t)u * pslot;
+        for (int x = tid; x < k * k; x += NT) {
+          const int pp = x / k, qq = x - pp * k;
+          if (qq >= pp) slot[pp * k - pp * (pp - 1) / 2 + (qq - pp)] = G[x];
+        }
+        for (int x = tid; x < k; x += NT) slot[k * (k + 1) / 2 + x] = bvec[x];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(&sp.done[hidx], 1) == nseg - 1;
+        __syncthreads();
+        if (!s_last) continue;
+        __threadfence();
+        for (int x = tid; x < k * k; x += NT) {
+          const int pp = x / k, qq = x - pp * k;
+          if (qq < pp) continue;
+          const int off = pp * k - pp * (pp - 1) / 2 + (qq - pp);
+          double acc = 0.0;
+          for (int sg = 0; sg < nseg; ++sg) acc += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + off);
+          G[x] = acc;
+        }
+        for (int x = tid; x < k; x += NT) {
+          double acc = 0.0;
+          for (int sg = 0; sg < nseg; ++sg)
+            acc += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + k * (k + 1) / 2 + x);
+          bvec[x] = acc;
+        }
+        if (tid == 0) sp.done[hidx] = 0;   // at rest for the next call
         __syncthreads();
       }
     } else {
@@ -513,6 +575,7 @@ size_t sort_temp_bytes(int n) {
 struct RowSched {
   int* order = nullptr;
   int* ticket = nullptr;   // [2], zeroed per call
+  const unsigned* deg = nullptr;   // degrees in that order
 };
 
 template <typename C>
@@ -540,8 +603,70 @@ int build_sched(const mfg_layout* lay, Carver& c, RowSched* rs, cudaStream_t str
   MFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(tmp, tmpb, kin, kout, rin, rs->order, n,
                                                            0, 32, stream));
   MFG_CUDA_CHECK(cudaMemsetAsync(rs->ticket, 0, 2 * sizeof(int), stream));
+  rs->deg = kout;
   return MFG_OK;
 }
+
+// Items of the split heavy rows from the sorted degrees (heavy rows are a
+// prefix of at most nnz/S <= grid rows; one 1024-thread block covers 2048).
+__global__ void __launch_bounds__(1024) k_split_items(const unsigned* __restrict__ deg, int n, int S,
+                                                      int4* __restrict__ items, int* __restrict__ info) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ int nh;
+  if (threadIdx.x == 0) nh = 0;
+  const int t0 = 2 * threadIdx.x;
+  int c[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int t = t0 + j;
+    const long long d = t < n ? (long long)deg[t] : 0;
+    c[j] = d > S ? (int)((d + S - 1) / S) : 0;
+  }
+  int off, agg;
+  Scan(ts).ExclusiveSum(c[0] + c[1], off, agg);
+  __syncthreads();
+  atomicAdd(&nh, (c[0] > 0) + (c[1] > 0));
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int base = off + (j ? c[0] : 0);
+    for (int sg = 0; sg < c[j]; ++sg) items[base + sg] = make_int4(t0 + j, sg, c[j], base);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    info[0] = nh;
+    info[1] = agg;
+  }
+}
+
+int split_len(int64_t nnz, int grid) {
+  const int64_t s = (nnz + grid - 1) / grid;
+  return (int)(s < 256 ? 256 : s);
+}
+
+template <typename C>
+void take_split(C& c, int grid, int k, SplitPlan* sp, int4** items, int** info) {
+  *items = c.template take<int4>((size_t)2 * grid);
+  *info = c.template take<int>(2);
+  sp->done = c.template take<int>(grid);
+  sp->part = c.template take<double>((size_t)2 * grid * (k * (k + 1) / 2 + k));
+}
+
+int build_split(const mfg_layout* lay, Carver& c, const RowSched& rs, int grid, int k, SplitPlan* sp,
+                cudaStream_t stream) {
+  int4* items;
+  int* info;
+  take_split(c, grid, k, sp, &items, &info);
+  MFG_REQUIRE(c.ok, "bcd workspace too small");
+  sp->S = split_len(lay->nnz, grid);
+  MFG_CUDA_CHECK(cudaMemsetAsync(sp->done, 0, sizeof(int) * grid, stream));
+  k_split_items<<<1, 1024, 0, stream>>>(rs.deg, lay->nrows, sp->S, items, info);
+  MFG_LAUNCH_CHECK();
+  sp->items = items;
+  sp->info = info;
+  return MFG_OK;
+}
+
 
 template <typename TS>
 int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, int ldo, double lam,
@@ -577,6 +702,9 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
   MFG_REQUIRE(c.ok, "bcd workspace too small");
   RowSched rs;
   if (int st = build_sched(lay, c, &rs, stream)) return st;
+  SplitPlan sp;
+  if (!global)
+    if (int st = build_split(lay, c, rs, grid, k, &sp, stream)) return st;
   const size_t smem = smem_bytes(k, global);
   if (smem > 48 * 1024) {
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -597,10 +725,11 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
   if (global)
     k_bcd<TS, kNTG><<<grid, kNTG, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo,
                                                  lam, (TS*)out, ldout, gs, 1, bad,
-                                                 smax >= 1 ? smax + 1 : 0, rs.order, rs.ticket + 1);
+                                                 smax >= 1 ? smax + 1 : 0, rs.order, rs.ticket + 1,
+                                                 SplitPlan{});
   else
     k_bcd<TS><<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
-                                           (TS*)out, ldout, gs, 0, bad, 0, rs.order, rs.ticket);
+                                           (TS*)out, ldout, gs, 0, bad, 0, rs.order, rs.ticket, sp);
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }
@@ -617,6 +746,12 @@ size_t bcd_workspace(const mfg_layout* lay, int k) {
   void* tmp;
   size_t tmpb;
   take_sched(s, lay ? lay->nrows : 0, &rs, &kin, &kout, &rin, &tmp, &tmpb);
+  if (k <= kSmemMaxK && lay) {
+    SplitPlan sp;
+    int4* items;
+    int* info;
+    take_split(s, grid_for_rows(lay->nrows), k, &sp, &items, &info);
+  }
   return s.off + 512;
 }
 

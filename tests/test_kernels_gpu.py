@@ -287,3 +287,38 @@ def test_bcd_large_k_packed_and_dual(k):
     w1, h1 = orc.bcd_epoch(om, w, h, 1.7)
     assert np.max(np.abs(_np(out.w) - w1)) < 1e-9 * max(1.0, np.abs(w1).max())
     assert np.max(np.abs(_np(out.h) - h1)) < 1e-9 * max(1.0, np.abs(h1).max())
+
+
+@pytest.mark.parametrize("k", [4, 20, 64, 128])
+def test_bcd_split_heavy_rows(k):
+    """Rows with more than S = max(256, nnz/grid) entries are cut into
+    segments whose partial Grams are summed in segment order by the CTA that
+    finishes the row (bcd.cu SplitPlan). A few rows here hold 600-3000
+    entries (2-12 segments) among many light ones, on both orientations;
+    the epoch must match the oracle's per-row normal equations, and a second
+    run must be bitwise identical (fixed reduction order)."""
+    rng = np.random.default_rng(100 + k)
+    m, n = 400, 3000
+    deg = rng.integers(1, 30, size=m)
+    deg[:6] = [3000, 2500, 1200, 800, 600, 257]
+    rows, cols = [], []
+    for i, d in enumerate(deg):
+        cc = rng.choice(n, size=d, replace=False)
+        if 7 not in cc:                  # column 7 in every row: a split CSC row too
+            cc = np.append(cc, 7)
+        rows.append(np.full(cc.size, i))
+        cols.append(cc)
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    perm = rng.permutation(m)           # heavy rows scattered, not first
+    r = perm[r]
+    v = rng.standard_normal(r.size)
+    om = orc.from_coo(m, n, r, c, v)
+    w = rng.standard_normal((m, k)) * 0.3
+    h = rng.standard_normal((n, k)) * 0.3
+    obs = D.ObservationSet.from_coo(m, n, r, c, v)
+    out = MF.bcd_epoch(obs, FactorPair(w, h), 1.3)
+    out2 = MF.bcd_epoch(obs, FactorPair(w, h), 1.3)
+    w1, h1 = orc.bcd_epoch(om, w, h, 1.3)
+    assert np.max(np.abs(_np(out.w) - w1)) < 1e-9 * max(1.0, np.abs(w1).max())
+    assert np.max(np.abs(_np(out.h) - h1)) < 1e-9 * max(1.0, np.abs(h1).max())
+    assert torch.equal(out.w, out2.w) and torch.equal(out.h, out2.h)
