@@ -80,6 +80,20 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   const int nhr = sp.items ? sp.info[0] : 0;   // split (heavy) rows: a prefix of the order
   const int nhi = sp.items ? sp.info[1] : 0;   // their segment items, taken first
   const int pslot = k * (k + 1) / 2 + k;       // packed upper Gram + rhs per segment
+  // Small k (at most NT/2 upper 4x4 tiles): EG groups of T threads each take
+  // every EG-th entry of the row for one tile, accumulating in registers
+  // across all chunks; the groups' partials are summed once per row in group
+  // order (fixed). With k = 20 that is 8 threads per tile instead of 1.
+  const int T = nt4 * (nt4 + 1) / 2;
+  const int EG = (!use_global && 2 * T <= NT) ? NT / T : 1;
+  int my_tp = 0, my_tq = 0, my_g = EG;      // my_g == EG: idle in the Gram
+  if (EG > 1 && tid < EG * T) {
+    my_g = tid / T;
+    int rem = tid - my_g * T;
+    while (rem >= nt4 - my_tp) { rem -= nt4 - my_tp; ++my_tp; }
+    my_tq = my_tp + rem;
+  }
+  double* red = G + k * k;                  // [EG][T][16] group partials (EG > 1)
   for (;;) {
     const int u = take_row(ticket, s_t, par);
     int i, seg = 0, nseg = 1, ibase = 0, hidx = -1, s0, s1;
@@ -100,6 +114,11 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
       for (int x = tid; x < k * k; x += NT) G[x] = 0.0;
     for (int x = tid; x < k; x += NT) bvec[x] = 0.0;
     __syncthreads();
+    double eacc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) eacc[a][b] = 0.0;
     if (!use_global) {
       for (int c0 = s0; c0 < s1; c0 += kc) {
         const int cn = min(kc, s1 - c0);
@@ -111,6 +130,23 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
         }
         for (int c = tid; c < kc; c += NT) sa[c] = c < cn ? (double)vals[c0 + c] : 0.0;
         __syncthreads();
+        if (EG > 1) {
+          if (my_g < EG) {
+            for (int c = my_g; c < cn; c += EG) {
+              double xp[4], xq[4];
+#pragma unroll
+              for (int a = 0; a < 4; ++a) {
+                const int p = my_tp * 4 + a, q = my_tq * 4 + a;
+                xp[a] = p < k ? stage[c * kp + p] : 0.0;
+                xq[a] = q < k ? stage[c * kp + q] : 0.0;
+              }
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) eacc[a][b] = fma(xp[a], xq[b], eacc[a][b]);
+            }
+          }
+        } else
         // Gram tiles (upper triangle incl. diagonal)
         for (int t = tid; t < nt4 * nt4; t += NT) {
           const int tp = t / nt4, tq = t - tp * nt4;
@@ -145,6 +181,28 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
           double s = 0.0;
           for (int c = 0; c < cn; ++c) s = fma(sa[c], stage[c * kp + d], s);
           bvec[d] += s;
+        }
+        __syncthreads();
+      }
+      if (EG > 1) {
+        if (my_g < EG) {
+          double* rp = red + ((size_t)my_g * T + (tid - my_g * T)) * 16;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) rp[a * 4 + b] = eacc[a][b];
+        }
+        __syncthreads();
+        if (my_g == 0) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              double v = 0.0;
+              for (int gg = 0; gg < EG; ++gg) v += red[((size_t)gg * T + tid) * 16 + a * 4 + b];
+              const int p = my_tp * 4 + a, q = my_tq * 4 + b;
+              if (p < k && q < k && q >= p) G[p * k + q] = v;
+            }
         }
         __syncthreads();
       }
@@ -544,7 +602,7 @@ size_t smem_bytes(int k, bool global) {
     if (gt > region) region = gt;
   }
   size_t n = region + 2 * (size_t)k;
-  if (!global) n += (size_t)k * k;
+  if (!global) n += (size_t)k * k + 16 * (size_t)kNT;   // + the group partials (small k)
   return n * sizeof(double);
 }
 
