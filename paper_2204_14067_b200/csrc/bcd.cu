@@ -19,7 +19,20 @@ namespace mfg {
 namespace {
 
 constexpr int kNT = 128;
-constexpr int kC = 16;         // entries staged per chunk
+constexpr int kC = 16;         // entries staged per chunk (packed/dual kernel)
+#ifndef MFG_BCD_KCS
+#define MFG_BCD_KCS 32
+#endif
+constexpr int kCS = MFG_BCD_KCS;  // entries per chunk of the small-k shared-memory path (fewer
+                                  // gather round trips and barriers per row)
+
+// Small-k shared-memory path (entry groups, see k_bcd): at most NT/2 upper
+// 4x4 tiles. Only it stages kCS entries per chunk and keeps the group
+// partials; larger k keeps kC-entry chunks and no partials buffer, since
+// the shared-memory footprint sets how many CTAs fit on an SM there.
+__host__ __device__ constexpr bool small_k_path(int k, int nt = kNT) {
+  return 2 * (((k + 3) / 4) * ((k + 3) / 4 + 1) / 2) <= nt;
+}
 constexpr int kSmemMaxK = 128; // Gram in shared memory up to this k
 constexpr int kNB = 32;        // panel width of the blocked Cholesky (global path)
 
@@ -52,7 +65,7 @@ __device__ __forceinline__ int take_row(int* ticket, int* s_t, int& par) {
 
 // 5 CTAs per SM at 128 threads (<= 102 registers): the split-row logic
 // otherwise raises the allocation to 124 registers and costs a CTA per SM
-template <typename TS, int NT = kNT>
+template <typename TS, int NT = kNT, bool SK = false>
 __global__ void __launch_bounds__(NT, NT == kNT ? 5 : 1)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
@@ -64,10 +77,13 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   // global path: the Cholesky panel [kNB][k] reuses the staging area, and
   // the Gram stages as many entries per chunk as that area holds (fewer
   // read-modify-write passes over the global Gram)
-  const int region0 = use_global && kNB * k > kC * kp + kC ? kNB * k : kC * kp + kC;
+  // SK: the small-k instantiation (entry groups); the others keep the plain
+  // tile loop, whose register allocation the groups' accumulators would crowd
+  const int kcs = SK ? kCS : kC;
+  const int region0 = use_global ? (kNB * k > kC * kp + kC ? kNB * k : kC * kp + kC) : kcs * kp + kcs;
   const int region = use_global && 32 * (64 + 4 * (NT / 16)) > region0 ? 32 * (64 + 4 * (NT / 16))
                                                                       : region0;
-  const int kc = use_global ? max(kC, min(64, region / (kp + 1))) : kC;  // entries per chunk
+  const int kc = use_global ? max(kC, min(64, region / (kp + 1))) : kcs;  // entries per chunk
   double* stage = sm;                           // [kc][kp]
   double* sa = stage + kc * kp;                 // [kc]
   double* bvec = sm + region;                   // [k]
@@ -85,7 +101,7 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
   // across all chunks; the groups' partials are summed once per row in group
   // order (fixed). With k = 20 that is 8 threads per tile instead of 1.
   const int T = nt4 * (nt4 + 1) / 2;
-  const int EG = (!use_global && 2 * T <= NT) ? NT / T : 1;
+  const int EG = SK ? NT / T : 1;
   int my_tp = 0, my_tq = 0, my_g = EG;      // my_g == EG: idle in the Gram
   if (EG > 1 && tid < EG * T) {
     my_g = tid / T;
@@ -130,7 +146,7 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
         }
         for (int c = tid; c < kc; c += NT) sa[c] = c < cn ? (double)vals[c0 + c] : 0.0;
         __syncthreads();
-        if (EG > 1) {
+        if constexpr (SK) {
           if (my_g < EG) {
             for (int c = my_g; c < cn; c += EG) {
               double xp[4], xq[4];
@@ -184,7 +200,7 @@ k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__
         }
         __syncthreads();
       }
-      if (EG > 1) {
+      if constexpr (SK) {
         if (my_g < EG) {
           double* rp = red + ((size_t)my_g * T + (tid - my_g * T)) * 16;
 #pragma unroll
@@ -595,14 +611,16 @@ constexpr int kNTG = 512;      // threads of the global (heavy-row) path: 16 war
 
 size_t smem_bytes(int k, bool global) {
   const int kp = k + 1;
-  size_t region = (size_t)kC * kp + kC;
+  const bool small = !global && small_k_path(k);
+  size_t region = small ? (size_t)kCS * kp + kCS : (size_t)kC * kp + kC;
   if (global) {
     if ((size_t)kNB * k > region) region = (size_t)kNB * k;
     const size_t gt = 32 * (64 + 4 * (kNTG / 16));
     if (gt > region) region = gt;
   }
   size_t n = region + 2 * (size_t)k;
-  if (!global) n += (size_t)k * k + 16 * (size_t)kNT;   // + the group partials (small k)
+  if (!global) n += (size_t)k * k;
+  if (small) n += 16 * (size_t)kNT;   // the entry groups' partials
   return n * sizeof(double);
 }
 
@@ -765,8 +783,10 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
     if (int st = build_split(lay, c, rs, grid, k, &sp, stream)) return st;
   const size_t smem = smem_bytes(k, global);
   if (smem > 48 * 1024) {
-    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNT, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNT, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNTG>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
@@ -786,8 +806,11 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
                                                  smax >= 1 ? smax + 1 : 0, rs.order, rs.ticket + 1,
                                                  SplitPlan{});
   else
-    k_bcd<TS><<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
-                                           (TS*)out, ldout, gs, 0, bad, 0, rs.order, rs.ticket, sp);
+  {
+    auto kern = small_k_path(k) ? k_bcd<TS, kNT, true> : k_bcd<TS, kNT, false>;
+    kern<<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
+                                      (TS*)out, ldout, gs, 0, bad, 0, rs.order, rs.ticket, sp);
+  }
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }
