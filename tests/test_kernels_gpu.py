@@ -289,14 +289,16 @@ def test_bcd_large_k_packed_and_dual(k):
     assert np.max(np.abs(_np(out.h) - h1)) < 1e-9 * max(1.0, np.abs(h1).max())
 
 
-@pytest.mark.parametrize("k", [4, 20, 64, 128])
+@pytest.mark.parametrize("k", [1, 4, 5, 20, 37, 40, 41, 64, 128])
 def test_bcd_split_heavy_rows(k):
     """Rows with more than S = max(256, nnz/grid) entries are cut into
     segments whose partial Grams are summed in segment order by the CTA that
     finishes the row (bcd.cu SplitPlan). A few rows here hold 600-3000
     entries (2-12 segments) among many light ones, on both orientations;
     the epoch must match the oracle's per-row normal equations, and a second
-    run must be bitwise identical (fixed reduction order)."""
+    run must be bitwise identical (fixed reduction order). k <= 40 takes the
+    small-k entry-group instantiation (bcd.cu small_k_path), 41 is the first
+    k on the plain path, and 1, 5, 37 leave a ragged last 4x4 tile."""
     rng = np.random.default_rng(100 + k)
     m, n = 400, 3000
     deg = rng.integers(1, 30, size=m)
