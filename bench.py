@@ -414,7 +414,7 @@ def main():
             cap = 6300 * 1.965e9 / 1e12
             l2 = {"bytes_per_launch": l2b, "achieved_TBps": l2b / (kern_ms * 1e-3) / 1e12,
                   "cap_TBps": cap, "frac": l2b / (kern_ms * 1e-3) / 1e12 / cap,
-                  "source": "lts__t_sectors.sum * 32 from profiles/r1g_*_k_sweep_g8f_full.json"}
+                  "source": "lts__t_sectors.sum * 32 from profiles/r1i_*_k_sweep_g8f_full.json"}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
