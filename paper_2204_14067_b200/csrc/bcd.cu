@@ -65,8 +65,11 @@ __device__ __forceinline__ int take_row(int* ticket, int* s_t, int& par) {
 
 // 5 CTAs per SM at 128 threads (<= 102 registers): the split-row logic
 // otherwise raises the allocation to 124 registers and costs a CTA per SM
+#ifndef MFG_BCD_SK_MINB
+#define MFG_BCD_SK_MINB 5
+#endif
 template <typename TS, int NT = kNT, bool SK = false>
-__global__ void __launch_bounds__(NT, NT == kNT ? 5 : 1)
+__global__ void __launch_bounds__(NT, NT == kNT ? (SK ? MFG_BCD_SK_MINB : 5) : 1)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
       int* __restrict__ bad, int min_d, const int* __restrict__ order, int* __restrict__ ticket,
