@@ -68,8 +68,13 @@ __device__ __forceinline__ int take_row(int* ticket, int* s_t, int& par) {
 #ifndef MFG_BCD_SK_MINB
 #define MFG_BCD_SK_MINB 5
 #endif
-template <typename TS, int NT = kNT, bool SK = false>
-__global__ void __launch_bounds__(NT, NT == kNT ? (SK ? MFG_BCD_SK_MINB : 5) : 1)
+// MINB: CTAs per SM the register allocation must allow. k <= kTinyK takes
+// the small-k instantiation with 8 (64 registers); its gathers need more
+// warps in flight, and the smaller Gram tiles leave the registers to spare
+// (profiles/r1i_bcd_minb_ab.log: c2 k=20 -10%; at k=30/40 8 CTAs cost 10-23%).
+constexpr int kTinyK = 24;
+template <typename TS, int NT = kNT, bool SK = false, int MINB = (SK ? MFG_BCD_SK_MINB : 5)>
+__global__ void __launch_bounds__(NT, NT == kNT ? MINB : 1)
 k_bcd(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
       double lam, TS* __restrict__ out, int ldout, double* __restrict__ gscratch, int use_global,
       int* __restrict__ bad, int min_d, const int* __restrict__ order, int* __restrict__ ticket,
@@ -790,6 +795,8 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNT, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNT, true, 8>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MFG_CUDA_CHECK(cudaFuncSetAttribute(k_bcd<TS, kNTG>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
@@ -810,7 +817,9 @@ int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, in
                                                  SplitPlan{});
   else
   {
-    auto kern = small_k_path(k) ? k_bcd<TS, kNT, true> : k_bcd<TS, kNT, false>;
+    auto kern = k <= kTinyK      ? k_bcd<TS, kNT, true, 8>
+                : small_k_path(k) ? k_bcd<TS, kNT, true>
+                                  : k_bcd<TS, kNT, false>;
     kern<<<grid, kNT, smem, stream>>>(*lay, k, (const TS*)vals, (const TS*)other, ldo, lam,
                                       (TS*)out, ldout, gs, 0, bad, 0, rs.order, rs.ticket, sp);
   }
