@@ -8,16 +8,20 @@ prints ONE JSON line on rank 0.
 
 A step = one Omega sweep over one instance at width k0:
 R = P_Omega(W H^T) - A, R.H (CSR), R^T.W (CSC), sum r^2, ||W||^2, ||H||^2.
-Default workload: BASELINE.json configs[1] (c2: 3706 x 6040 canonical,
-|Omega| = 1,000,209, k0 = 20, fp32 values, fp64 reductions), synthetic
-(seeded Zipf generator, paper_2204_14067_b200/synth.py).
+Default workload: BASELINE.json configs[3] (c4: 17,770 x 480,189 canonical,
+|Omega| = 100,480,507, k0 = 40, fp32 values, fp64 reductions), the largest
+configuration that fits one GPU and the one BASELINE.json quotes at
+1/2/4/8 B200; synthetic (seeded Zipf generator,
+paper_2204_14067_b200/synth.py).
 
 Timing: W untimed warm-up steps, then K timed steps bracketed by barrier +
 synchronize; each step is timed with CUDA events on the launching stream and
 L2 is flushed (512 MiB write, outside the events) before every step, since
-the c2 working set (~30 MB) fits in the 126 MB L2. Multi-GPU (torchrun): each
-rank sweeps its own instance (independent partitions, weak scaling, no
-collective on the data path); the reported time is the max over ranks.
+the factors of the smaller configs fit in the 126 MB L2. Multi-GPU
+(torchrun): by default the ranks sweep row/column shards of ONE instance
+(strong scaling: no data-path collective for the sweep,
+all-gathers of W/H blocks in the BCD epoch line); ``--independent`` runs one
+instance per rank instead (weak scaling). Times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -47,14 +51,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="bounded CPU-baseline sample (seconds of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tto", action="store_true", help="skip the time-to-objective leg")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: the ranks sweep row/column shards of ONE instance "
-                         "(mfg_sweep_sharded, no data-path collective) instead of one instance each")
+                         "(mfg_sweep_sharded, no data-path collective); the default for N > 1")
+    ap.add_argument("--independent", action="store_true",
+                    help="N > 1: one independent instance per rank (weak scaling) instead of shards")
+    ap.add_argument("--no-bcd", action="store_true", help="skip the BCD-epoch leg")
     ap.add_argument("--sweep", default="grouped", choices=["grouped", "staged"],
                     help="sweep kernel: all-gather grouped (k_sweep_g8f) or shared-memory staged")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
@@ -190,57 +197,157 @@ def time_to_objective(target_rel: float = 1e-6):
             "run_seconds": total, "omega_build_seconds": t_build,
             "final_rank": trace.final().rank,
             "reference_seconds": ref_hit, "reference_run_seconds": ref.get("elapsed_s"),
-            "reference_note": "reference timings from its own run in the build container "
-                              "(8 CPU cores, tests/golden/make_golden.py --c1)"}
+            "reference_same_box": False,
+        "reference_note": "reference timings come from its own run in the build container "
+                          "(8 CPU cores, tests/golden/make_golden.py --c1), NOT from this "
+                          "box's host: the 560 s reference run does not fit the bench budget"}
 
 
-def cpu_sweep_setup(m, n, r, c, v, k):
-    from oracle import mfg_oracle as orc
-    from paper_2204_14067_b200 import synth
-
-    om = orc.from_coo(m, n, r, c, v)
-    w, h = synth.sweep_factors(m, n, k, seed=1, dtype=np.float32)
-    w, h = w.astype(np.float64), h.astype(np.float64)
-    return orc, om, w, h
+_CPU = None  # the CpuSweep whose arrays forked pool workers inherit
 
 
-def cpu_sweep_port(orc, om, w, h, perm, csc):
-    """The reference's sweep (pair_values einsum + scipy CSR/CSC SpMM) with the
-    CSR/CSC index caches prebuilt, as SURVEY.md §8(d) prescribes."""
-    import scipy.sparse as sp
+def _cpu_worker_init():
+    # one BLAS thread per worker process (the pool supplies the parallelism;
+    # OpenBLAS's own threads would oversubscribe the cores)
+    from threadpoolctl import threadpool_limits
 
-    r = orc.pair_values(w, h, om.rows, om.cols) - om.vals
-    rh = sp.csr_matrix((r, om.cols, om.indptr), shape=(om.m, om.n)) @ h
-    rt = sp.csr_matrix((r[perm], csc.indices, csc.indptr), shape=(om.n, om.m))
-    rtw = rt @ w
-    return r, rh, rtw, float(r @ r), float(np.sum(w * w)), float(np.sum(h * h))
+    threadpool_limits(1)
+
+
+def _cpu_task(t):
+    kind, a, b = t
+    if kind == 0:
+        return _CPU._csr_block(a, b)
+    return _CPU._csc_block(a, b)
+
+
+class CpuSweep:
+    """The reference's CPU sweep (SURVEY.md §8(d) unit) restated with its own
+    calls -- numpy einsum SDDMM (``pair_values``, mfg/data.py:253-263) + scipy
+    CSR SpMM ``grad.csr @ H`` and CSC SpMM ``grad.csr_t @ W``
+    (mfg/operators.py:108,117) -- timed on a bounded sample of the workload
+    on every host core.
+
+    A sample of fraction f is the CSR rows [0, i1) and the CSC rows (= Omega
+    columns) [0, j1) that each hold ~f of the entries: SDDMM + R.H over the
+    CSR rows, R^T.W over the CSC rows (their r values come from the same
+    SDDMM, which the reference computes once per sweep, so they are prepared
+    outside the timed region). The CSR/CSC index caches are prebuilt, as the
+    survey prescribes. Row ranges are split into 4 blocks per core and run on
+    a fork()ed process pool with one BLAS thread per process; the reference
+    itself calls them single-threaded. Create it before CUDA is initialised."""
+
+    def __init__(self, m, n, r, c, v, k, procs=None):
+        from oracle import mfg_oracle as orc
+        from paper_2204_14067_b200 import synth
+
+        self.orc = orc
+        self.om = om = orc.from_coo(m, n, r, c, v)
+        w, h = synth.sweep_factors(m, n, k, seed=1, dtype=np.float32)
+        self.w, self.h = w.astype(np.float64), h.astype(np.float64)
+        self.perm = om.csc_perm()
+        self.cptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(np.bincount(om.cols, minlength=n), out=self.cptr[1:])
+        self.crow = om.rows[self.perm]          # CSC row ids (= csr_t indices)
+        self.procs = procs or len(os.sched_getaffinity(0))
+        self.pool = None
+        self.frac = 0.0
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.terminate()
+            self.pool.join()
+            self.pool = None
+
+    def set_fraction(self, f: float):
+        import multiprocessing as mp
+
+        global _CPU
+        om = self.om
+        f = min(max(f, 0.0), 1.0)
+        nnz = om.size
+        self.i1 = int(np.searchsorted(om.indptr, f * nnz, side="left")) if f < 1 else om.m
+        self.j1 = int(np.searchsorted(self.cptr, f * nnz, side="left")) if f < 1 else om.n
+        self.i1, self.j1 = max(self.i1, 1), max(self.j1, 1)
+        e1 = int(self.cptr[self.j1])
+        sel = self.perm[:e1]
+        # the sample's CSC-side residuals (computed once per sweep by the reference)
+        self.r_csc = self.orc.pair_values(self.w, self.h, om.rows[sel], om.cols[sel]) - om.vals[sel]
+        self.frac = (int(om.indptr[self.i1]) + e1) / (2.0 * max(nnz, 1))
+        nb = 4 * self.procs
+        ei = np.unique(np.linspace(0, self.i1, nb + 1).astype(np.int64))
+        ej = np.unique(np.linspace(0, self.j1, nb + 1).astype(np.int64))
+        self.tasks = ([(0, int(a), int(b)) for a, b in zip(ei[:-1], ei[1:])]
+                      + [(1, int(a), int(b)) for a, b in zip(ej[:-1], ej[1:])])
+        self.close()
+        _CPU = self
+        self.pool = mp.get_context("fork").Pool(self.procs, initializer=_cpu_worker_init)
+        self.pool.map(_cpu_task, [(0, 0, 1)] * self.procs)  # workers up
+        return self.frac
+
+    def _csr_block(self, i0, i1):
+        import scipy.sparse as sp
+
+        om = self.om
+        lo, hi = int(om.indptr[i0]), int(om.indptr[i1])
+        r = self.orc.pair_values(self.w, self.h, om.rows[lo:hi], om.cols[lo:hi]) - om.vals[lo:hi]
+        g = sp.csr_matrix((r, om.cols[lo:hi], om.indptr[i0:i1 + 1] - lo), shape=(i1 - i0, om.n))
+        rh = g @ self.h
+        return float(r @ r) + float(rh[0, 0] if rh.size else 0.0)
+
+    def _csc_block(self, j0, j1):
+        import scipy.sparse as sp
+
+        lo, hi = int(self.cptr[j0]), int(self.cptr[j1])
+        g = sp.csr_matrix((self.r_csc[lo:hi], self.crow[lo:hi], self.cptr[j0:j1 + 1] - lo),
+                          shape=(j1 - j0, self.om.m))
+        rtw = g @ self.w
+        return float(rtw[0, 0] if rtw.size else 0.0)
+
+    def step(self) -> float:
+        """One timed sample; returns its wall seconds."""
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_task, self.tasks, chunksize=1)
+        return time.perf_counter() - t0
+
+    def calibrate(self, step_seconds: float, f_min: float = 1e-3) -> float:
+        """Pick the sample fraction so that one step takes ~step_seconds."""
+        f = self.set_fraction(max(f_min, min(1.0, 1e6 / max(self.om.size, 1))))
+        t = min(self.step() for _ in range(2))
+        if f < 1.0 or t > step_seconds:
+            f = self.set_fraction(min(1.0, max(f_min, f * step_seconds / max(t, 1e-6))))
+        return f
+
+    def describe(self, steps: int) -> str:
+        return (f"{steps} samples of {100 * self.frac:.2f}% of the sweep each (CSR rows "
+                f"[0,{self.i1}) + CSC rows [0,{self.j1}); numpy einsum SDDMM + scipy CSR/CSC "
+                f"SpMM over row blocks on {self.procs} host processes); value = sampled "
+                "fraction / step time, in full sweeps/s")
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
+    """--impl reference: the reference's CPU path (oracle port of its own
+    calls) on the host cores, rank 0 only; each step a bounded sample."""
     if rank != 0:
         return
     m, n, r, c, v, spec = instance(args.workload, seed=0)
-    orc, om, w, h = cpu_sweep_setup(m, n, r, c, v, spec.k0)
-    perm = om.csc_perm()
-    csc = om.a_csr_t
+    cs = CpuSweep(m, n, r, c, v, spec.k0)
+    budget = float(os.environ.get("MFG_REF_BUDGET_S", "90"))
+    cs.calibrate(budget / max(args.steps + args.warmup, 1))
     for _ in range(args.warmup):
-        cpu_sweep_port(orc, om, w, h, perm, csc)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        cpu_sweep_port(orc, om, w, h, perm, csc)
-    el = time.perf_counter() - t0
-    value = args.steps / el
+        cs.step()
+    el = sum(cs.step() for _ in range(args.steps))
+    cs.close()
+    value = args.steps * cs.frac / el
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": args.workload, "m": m, "n": n, "nnz": int(om.size), "k": spec.k0},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} full {args.workload} sweeps (numpy einsum "
-                                   "SDDMM + scipy CSR/CSC SpMM; single-threaded like the "
-                                   "reference's sparse calls)"},
+        "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": args.workload, "m": m, "n": n, "nnz": int(cs.om.size),
+                   "k": spec.k0},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cs.procs, "kind": "port",
+                         "sample": cs.describe(args.steps)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -254,7 +361,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.shard:
+    if args.shard or (world > 1 and not args.independent):
         main_shard(args, rank, world, local_rank)
         return
 
@@ -265,14 +372,27 @@ def main():
     from paper_2204_14067_b200.data import ObservationSet
     from paper_2204_14067_b200.mfsolver import SweepPlan
 
+    m, n, r, c, v, spec = instance(args.workload, seed=rank)
+    k = spec.k0
+    # CPU baseline first: its process pool is fork()ed before CUDA initialises
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cs = CpuSweep(m, n, r, c, v, k)
+        cs.calibrate(args.cpu_seconds / 4)
+        el, cnt_cpu = 0.0, 0
+        while el < args.cpu_seconds and cnt_cpu < 1000:
+            el += cs.step()
+            cnt_cpu += 1
+        cpu = {"value": cnt_cpu * cs.frac / el, "unit": UNIT, "cores": cs.procs,
+               "kind": "port", "sample": cs.describe(cnt_cpu)}
+        cs.close()
+        del cs
+
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
     lib = _lib.lib()
-
-    m, n, r, c, v, spec = instance(args.workload, seed=rank)
-    k = spec.k0
     obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
     w_np, h_np = synth.sweep_factors(m, n, k, seed=1 + rank, dtype=np.float32)
     t_plan = time.perf_counter()
@@ -416,23 +536,9 @@ def main():
                   "cap_TBps": cap, "frac": l2b / (kern_ms * 1e-3) / 1e12 / cap,
                   "source": "lts__t_sectors.sum * 32 from profiles/r1i_*_k_sweep_g8f_full.json"}
 
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        orc, om, wc, hc = cpu_sweep_setup(m, n, r, c, v, k)
-        perm = om.csc_perm()
-        csc = om.a_csr_t
-        t0 = time.perf_counter()
-        cnt_cpu = 0
-        while True:
-            cpu_sweep_port(orc, om, wc, hc, perm, csc)
-            cnt_cpu += 1
-            el = time.perf_counter() - t0
-            if el >= args.cpu_seconds or cnt_cpu >= 1000:
-                break
-        cpu = {"value": cnt_cpu / el, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{cnt_cpu} full {args.workload} sweeps on the host "
-                         f"({os.cpu_count()} cores visible; the reference's einsum/scipy "
-                         "sparse calls are single-threaded)"}
+    bcd = None
+    if not args.no_bcd and world == 1:
+        bcd = bcd_epoch_leg(args, m, n, r, c, v, k, rank, world, dev, spec)
 
     tto = None
     if not args.no_tto and world == 1:
@@ -442,13 +548,14 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 reductions)",
-        "data": "synthetic",
+        "data": "synthetic (seeded Zipf instance with the config's shape; no dataset records)",
         "config": {"workload": args.workload, "m": m, "n": n, "nnz": int(obs.size), "k": k,
                    "values": "fp32", "l2": {"write": "flushed before every step (512 MiB write)",
                           "read": "flushed before every step (512 MiB read)",
                           "none": "not flushed (L2-warm)"}[args.flush],
                    "timing": "per-step CUDA events, CUDA-graph replay of the sweep",
-                   "parallelism": f"{world} independent partitions (one per GPU)",
+                   "parallelism": (f"{world} independent instances (one per GPU)" if world > 1
+                                   else "1 GPU"),
                    "sweep": args.sweep, "plan_seconds": round(t_plan, 3),
                    **({"staged": plan.staged.stats()} if plan.staged is not None else {})},
         "e2e": {"value": e2e_value, "unit": UNIT,
@@ -466,10 +573,58 @@ def main():
         "cpu_baseline": cpu,
         "clocks": clocks,
         "time_to_objective": tto,
+        "bcd_epoch": bcd,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bcd_epoch_leg(args, m, n, r, c, v, k, rank, world, dev, spec, shard=None):
+    """One BCD epoch (mfg/mfsolver.py:78-93) over the rank's row/column shards
+    of the instance, including the all-gathers of the W and H blocks
+    (SURVEY.md §8(e)); fp32 factors, fp64 per-row Gram + Cholesky. Timed with
+    CUDA events (max over ranks), 1 warm-up + 3 timed epochs."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_14067_b200 import sharding, synth
+
+    if shard is None:
+        shard = sharding.make_shard(m, n, r, c, v, rank, world)
+    mf = sharding.ShardedMF(shard, sharding.DeviceOps(torch.float32), sharding.Comm(), dev)
+    w_np, h_np = synth.sweep_factors(m, n, k, seed=1, dtype=np.float32)
+    w = torch.as_tensor(w_np, device=dev)
+    h = torch.as_tensor(h_np, device=dev)
+    lam = float(spec.lam)
+    mf.bcd_epoch(w, h, lam)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ms = []
+    for _ in range(3):
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        w2, h2 = mf.bcd_epoch(w, h, lam)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = torch.tensor([min(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_epoch = float(t.item())
+    if not (torch.isfinite(w2).all() and torch.isfinite(h2).all()):
+        raise RuntimeError("non-finite BCD epoch")
+    nnz = len(v)
+    flops = 2.0 * nnz * k * (k + 1)   # SURVEY §8(d): row-Gram assembly per epoch
+    del mf
+    torch.cuda.empty_cache()
+    return {"ms_per_epoch": ms_epoch, "epochs_per_s": 1e3 / ms_epoch, "lam": lam, "k": k,
+            "gram_flops": flops, "gram_tflops": flops / (ms_epoch * 1e-3) / 1e12,
+            "timing": "best of 3 epochs (after 1 warm-up), CUDA events, max over ranks",
+            "parallelism": (f"{world} row/column shards, W and H blocks all-gathered (NCCL)"
+                            if world > 1 else "1 GPU")}
 
 
 def main_shard(args, rank, world, local_rank):
@@ -580,6 +735,9 @@ def main_shard(args, rank, world, local_rank):
     sums = plan.sums.cpu().numpy()
     if not np.all(np.isfinite(sums)):
         raise RuntimeError("non-finite sweep sums")
+    bcd = None
+    if not args.no_bcd:
+        bcd = bcd_epoch_leg(args, m, n, r, c, v, k, rank, world, dev, spec, shard=shard)
     if rank == 0:
         nnz_r, nnz_c = obs_r.size, obs_c.size
         kb = int(nnz_r * 16 + nnz_c * 12 + 0.125 * (nnz_r + nnz_c)
@@ -595,7 +753,7 @@ def main_shard(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 (fp64 reductions)",
-            "data": "synthetic",
+            "data": "synthetic (seeded Zipf instance with the config's shape; no dataset records)",
             "config": {"workload": args.workload, "m": m, "n": n, "nnz": len(v), "k": k,
                        "values": "fp32", "l2": "flushed before every step (512 MiB write)",
                        "timing": "per-step CUDA events, CUDA-graph replay, max over ranks",
@@ -614,6 +772,7 @@ def main_shard(args, rank, world, local_rank):
                          "peak_source": peak_src},
             "cpu_baseline": None,
             "clocks": clocks,
+            "bcd_epoch": bcd,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
