@@ -62,8 +62,6 @@ def parse():
     ap.add_argument("--independent", action="store_true",
                     help="N > 1: one independent instance per rank (weak scaling) instead of shards")
     ap.add_argument("--no-bcd", action="store_true", help="skip the BCD-epoch leg")
-    ap.add_argument("--sweep", default="grouped", choices=["grouped", "staged"],
-                    help="sweep kernel: all-gather grouped (k_sweep_g8f) or shared-memory staged")
     ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
                     help="L2 flush between steps: write (zero 512 MiB), read (sum 512 MiB) or none")
     return ap.parse_args()
@@ -396,7 +394,7 @@ def main():
     obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
     w_np, h_np = synth.sweep_factors(m, n, k, seed=1 + rank, dtype=np.float32)
     t_plan = time.perf_counter()
-    plan = SweepPlan(obs, k, compute_f64=False, staged=args.sweep == "staged")
+    plan = SweepPlan(obs, k, compute_f64=False)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     # resident factors in the grouped kernel layout (unpadded when k allows)
@@ -528,7 +526,7 @@ def main():
             tj = json.load(fh)
         traffic = tj.get(args.workload)
         l2b = tj.get("l2_bytes", {}).get(args.workload)
-        if l2b and plan.staged is None:
+        if l2b:
             # bytes through L2 per launch (ncu capture) over the live kernel time,
             # against the LTS throughput cap (~6300 B/cycle at the max SM clock)
             cap = 6300 * 1.965e9 / 1e12
@@ -556,16 +554,14 @@ def main():
                    "timing": "per-step CUDA events, CUDA-graph replay of the sweep",
                    "parallelism": (f"{world} independent instances (one per GPU)" if world > 1
                                    else "1 GPU"),
-                   "sweep": args.sweep, "plan_seconds": round(t_plan, 3),
-                   **({"staged": plan.staged.stats()} if plan.staged is not None else {})},
+                   "plan_seconds": round(t_plan, 3)},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": int((m + n) * k * 4),
                 "d2h_bytes_per_step": int(plan._host.numel())},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("k_sweep_g8f (fused CSR+CSC pass)" if plan.staged is None else
-                                "k_sweep_staged + k_staged_fold (timed together)"),
+                     "kernel": "k_sweep_g8f (fused CSR+CSC pass)",
                      "bytes_per_launch": kb, "avg_launch_us": kern_ms * 1e3,
                      "peak_source": peak_src,
                      "survey_unfused_bytes": survey_bytes(obs.size, m, n, k, 4),

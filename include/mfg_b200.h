@@ -162,71 +162,6 @@ int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr,
               int ldh, void* R, void* RH, void* RtW, double out_scale,
               double* sums, void* workspace, size_t ws_bytes, void* stream);
 
-/* ---- The staged (shared-memory tiled) sweep, fp32 -----------------------
- * Same outputs as mfg_sweep (R in CSR order, RH, RtW, sums) for fp32
- * storage and arithmetic with fp64 sums, over a plan that reorders each
- * orientation's entries by (factor block, output row, col): the gathered
- * factor's rows, ranked by degree, are cut into blocks of S rows
- * (mfg_staged_block_rows(k)) that one CTA stages into shared memory, so
- * entries of a staged block gather their factor rows from shared memory;
- * the remaining "cold" entries gather from global memory. A worker's run of
- * entries of one output row inside its chunk is a piece; its partial row of
- * R.H is written to a piece buffer and a fold kernel sums the pieces of
- * every output row in stream order (deterministic). Plans are built by
- * paper_2204_14067_b200.staged.StagedPlan (host-side planning on the
- * device with torch); all arrays below are device arrays.
- * Replaces the same reference calls as mfg_sweep (mfg/data.py:253-293,
- * mfg/operators.py:53-55,108,117).                                        */
-typedef struct {
-  int32_t nrows;            /* output rows (m for the CSR pass, n for CSC)      */
-  int32_t S;                /* rows per staged block                            */
-  int64_t nstream;          /* stream length incl. 32-alignment gaps            */
-  const int32_t* sidx;      /* [nstream+64] block slot, or gathered row (cold)  */
-  const int32_t* srow;      /* [nstream+64] output row                          */
-  const int32_t* prow;      /* [npieces+3] output row of each piece (+ padding) */
-  const float* svals;       /* [nstream+64] A                                   */
-  const int32_t* spos;      /* [nstream+64] CSR position (R index; CSR pass)    */
-  const uint32_t* bmask;    /* [nstream/32+1] bit: entry starts an output row   */
-  const int32_t* members;   /* [nblocks*S] gathered row of each block slot      */
-  int32_t nblocks;
-  int32_t npieces;
-  const int32_t* pptr;      /* [nrows+1] pieces of row i: plist[pptr[i]..]      */
-  const int32_t* plist;     /* [npieces] piece ids, stream order per row        */
-} mfg_staged_pass;
-
-typedef struct {
-  mfg_staged_pass pass[2];  /* [0] CSR: self W, gathers H; [1] CSC: self H, gathers W */
-  int32_t k;
-  int32_t grid;             /* CTAs (one per SM); tiles are handed out by tickets */
-  int32_t nchunks;
-  int32_t ntiles;
-  const int32_t* chunks;    /* [nchunks][4] E0, E1 (stream), first piece, pass  */
-  const int32_t* tiles;     /* [ntiles][4] pass, block (-1 cold), chunk begin, end;
-                               end - begin <= mfg_staged_workers(k)           */
-  const int32_t* tile_nblk; /* [ntiles] 32-entry blocks per chunk               */
-  int32_t l1;               /* 1: L1-blocked plan (block-ordered stream, nothing
-                               staged: every tile gathers through L1)         */
-} mfg_staged_plan;
-
-/* rows of a staged block for width k (0 if k is not supported: k > 64)      */
-int mfg_staged_block_rows(int k);
-/* 8-lane workers per CTA for width k (chunks per tile; 0 if unsupported)   */
-int mfg_staged_workers(int k);
-size_t mfg_sweep_staged_workspace(const mfg_staged_plan* plan);
-/* W (m x k, ld ldw), H (n x k, ld ldh): ld multiples of 4, padding zero.
- * RH (m x k) and RtW (n x k) are dense (ld = k); R may be NULL.           */
-int mfg_sweep_staged(const mfg_staged_plan* plan, const float* W, int ldw,
-                     const float* H, int ldh, float* R, float* RH, float* RtW,
-                     double out_scale, double* sums, void* workspace,
-                     size_t ws_bytes, void* stream);
-/* end-to-end variant (see mfg_sweep_host): H2D of W_host/H_host into W/H,
- * the staged sweep, one D2H of out = [sums (32 B) | RH | RtW].            */
-int mfg_sweep_staged_host(const mfg_staged_plan* plan, const float* W_host,
-                          const float* H_host, float* W, int ldw, float* H,
-                          int ldh, float* R, void* out, void* out_host,
-                          double out_scale, void* workspace, size_t ws_bytes,
-                          void* stream);
-
 /* ---- SDDMM with fused reductions --------------------------------------
  * p_e = sum_d L[row_e, d] * (scale ? scale[d] : 1) * Rt[col_e, d]
  * r_e = p_e - A_e (A may be NULL -> 0)
@@ -263,6 +198,13 @@ int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k,
                        const void* vals, const void* other, int ldo,
                        double lam, void* out, int ldout, void* workspace,
                        size_t ws_bytes, void* stream);
+/* Enqueue (on `stream`) a copy of the last half-sweep's status word from its
+ * workspace into *flag_host (pinned host memory for an asynchronous copy):
+ * nonzero when a Cholesky pivot was <= 0 or NaN (a non-SPD normal matrix,
+ * i.e. non-finite factors or values), which the reference's batched
+ * np.linalg.solve (mfg/mfsolver.py:75) would turn into NaN rows. The Python
+ * layer raises NumericalError (mfg/driver.py:52) for it.                   */
+int mfg_bcd_status(const void* workspace, int* flag_host, void* stream);
 
 /* ---- dense reductions ---------------------------------------------------
  * sums_host-free fp64 dot: out[0] = sum_i x_i y_i over `count` entries.    */

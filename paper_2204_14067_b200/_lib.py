@@ -42,43 +42,6 @@ class Layout(ctypes.Structure):
     ]
 
 
-class StagedPass(ctypes.Structure):
-    """mirror of ``mfg_staged_pass`` (include/mfg_b200.h)."""
-
-    _fields_ = [
-        ("nrows", ctypes.c_int32),
-        ("S", ctypes.c_int32),
-        ("nstream", ctypes.c_int64),
-        ("sidx", ctypes.c_void_p),
-        ("srow", ctypes.c_void_p),
-        ("prow", ctypes.c_void_p),
-        ("svals", ctypes.c_void_p),
-        ("spos", ctypes.c_void_p),
-        ("bmask", ctypes.c_void_p),
-        ("members", ctypes.c_void_p),
-        ("nblocks", ctypes.c_int32),
-        ("npieces", ctypes.c_int32),
-        ("pptr", ctypes.c_void_p),
-        ("plist", ctypes.c_void_p),
-    ]
-
-
-class StagedPlanC(ctypes.Structure):
-    """mirror of ``mfg_staged_plan`` (include/mfg_b200.h)."""
-
-    _fields_ = [
-        ("pass_", StagedPass * 2),
-        ("k", ctypes.c_int32),
-        ("grid", ctypes.c_int32),
-        ("nchunks", ctypes.c_int32),
-        ("ntiles", ctypes.c_int32),
-        ("chunks", ctypes.c_void_p),
-        ("tiles", ctypes.c_void_p),
-        ("tile_nblk", ctypes.c_void_p),
-        ("l1", ctypes.c_int32),
-    ]
-
-
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
@@ -86,7 +49,6 @@ _INT = ctypes.c_int
 _D = ctypes.c_double
 _SZ = ctypes.c_size_t
 _LP = ctypes.POINTER(Layout)
-_SP = ctypes.POINTER(StagedPlanC)
 
 _SIGS = {
     "mfg_last_error": (ctypes.c_char_p, []),
@@ -109,11 +71,6 @@ _SIGS = {
                                  _P, _P, _D, _P, _P, _SZ, _P]),
     "mfg_sweep_host": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _P, _P, _INT, _P, _INT, _P,
                               _P, _P, _D, _P, _SZ, _P]),
-    "mfg_staged_block_rows": (_INT, [_INT]),
-    "mfg_staged_workers": (_INT, [_INT]),
-    "mfg_sweep_staged_workspace": (_SZ, [_SP]),
-    "mfg_sweep_staged": (_INT, [_SP, _P, _INT, _P, _INT, _P, _P, _P, _D, _P, _P, _SZ, _P]),
-    "mfg_sweep_staged_host": (_INT, [_SP, _P, _P, _P, _INT, _P, _INT, _P, _P, _P, _D, _P, _SZ, _P]),
     "mfg_sddmm_workspace": (_SZ, [_LP, _INT]),
     "mfg_sddmm": (_INT, [_INT, _INT, _LP, _INT, _P, _INT, _P, _P, _INT, _P, _P, _D, _P, _P, _P,
                          _SZ, _P]),
@@ -121,6 +78,7 @@ _SIGS = {
     "mfg_spmm": (_INT, [_INT, _LP, _INT, _P, _P, _INT, _D, _D, _P, _INT, _P, _SZ, _P]),
     "mfg_bcd_workspace": (_SZ, [_LP, _INT]),
     "mfg_bcd_half_sweep": (_INT, [_INT, _LP, _INT, _P, _P, _INT, _D, _P, _INT, _P, _SZ, _P]),
+    "mfg_bcd_status": (_INT, [_P, _P, _P]),
     "mfg_dot": (_INT, [_INT, _I64, _P, _P, _P, _P, _SZ, _P]),
     "mfg_profile_enable": (_INT, [_INT]),
     "mfg_profile_collect": (_INT, [ctypes.POINTER(_D), ctypes.POINTER(_INT)]),

@@ -167,50 +167,6 @@ extern "C" int mfg_sweep_host(int dtype, int compute_f64, const mfg_layout* csr,
   return MFG_OK;
 }
 
-extern "C" int mfg_staged_block_rows(int k) { return staged_block_rows(k); }
-extern "C" int mfg_staged_workers(int k) { return staged_workers(k); }
-
-extern "C" size_t mfg_sweep_staged_workspace(const mfg_staged_plan* plan) {
-  return plan ? staged_workspace(plan) : 0;
-}
-
-extern "C" int mfg_sweep_staged(const mfg_staged_plan* plan, const float* W, int ldw,
-                                const float* H, int ldh, float* R, float* RH, float* RtW,
-                                double out_scale, double* sums, void* workspace, size_t ws_bytes,
-                                void* stream) {
-  MFG_REQUIRE(plan, "null plan");
-  return staged_sweep(plan, W, ldw, H, ldh, R, RH, RtW, out_scale, sums, workspace, ws_bytes,
-                      (cudaStream_t)stream);
-}
-
-extern "C" int mfg_sweep_staged_host(const mfg_staged_plan* plan, const float* W_host,
-                                     const float* H_host, float* W, int ldw, float* H, int ldh,
-                                     float* R, void* out, void* out_host, double out_scale,
-                                     void* workspace, size_t ws_bytes, void* stream) {
-  MFG_REQUIRE(plan, "null plan");
-  MFG_REQUIRE(W_host && H_host && W && H && out, "null buffer");
-  const int k = plan->k;
-  MFG_REQUIRE(k >= 1 && ldw >= k && ldh >= k, "need k >= 1 and ldw, ldh >= k");
-  const cudaStream_t st = (cudaStream_t)stream;
-  const size_t m = (size_t)plan->pass[0].nrows, n = (size_t)plan->pass[1].nrows, es = 4;
-  auto h2d = [&](void* dst, int ld, const void* src, size_t rows) -> cudaError_t {
-    if (rows == 0) return cudaSuccess;
-    if ((size_t)ld == (size_t)k)
-      return cudaMemcpyAsync(dst, src, rows * k * es, cudaMemcpyHostToDevice, st);
-    return cudaMemcpy2DAsync(dst, ld * es, src, k * es, k * es, rows, cudaMemcpyHostToDevice, st);
-  };
-  MFG_CUDA_CHECK(h2d(W, ldw, W_host, m));
-  MFG_CUDA_CHECK(h2d(H, ldh, H_host, n));
-  char* o = static_cast<char*>(out);
-  const int rc = staged_sweep(plan, W, ldw, H, ldh, R, reinterpret_cast<float*>(o + 32),
-                              reinterpret_cast<float*>(o + 32 + m * k * es), out_scale,
-                              reinterpret_cast<double*>(o), workspace, ws_bytes, st);
-  if (rc != MFG_OK) return rc;
-  if (out_host)
-    MFG_CUDA_CHECK(cudaMemcpyAsync(out_host, out, 32 + (m + n) * k * es, cudaMemcpyDeviceToHost, st));
-  return MFG_OK;
-}
-
 extern "C" size_t mfg_sddmm_workspace(const mfg_layout* lay, int k) {
   return sddmm_workspace(lay, k);
 }
@@ -253,6 +209,14 @@ extern "C" int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k, const
   MFG_REQUIRE(lam > 0.0, "lam must be positive");
   return bcd_dispatch(dtype, lay, k, vals, other, ldo, lam, out, ldout, workspace, ws_bytes,
                       (cudaStream_t)stream);
+}
+
+extern "C" int mfg_bcd_status(const void* workspace, int* flag_host, void* stream) {
+  MFG_REQUIRE(workspace && flag_host, "null workspace or flag");
+  // the half-sweep's non-SPD flag is the workspace's first word (bcd.cu do_bcd)
+  MFG_CUDA_CHECK(cudaMemcpyAsync(flag_host, workspace, sizeof(int), cudaMemcpyDeviceToHost,
+                                 (cudaStream_t)stream));
+  return MFG_OK;
 }
 
 extern "C" int mfg_dot(int dtype, int64_t count, const void* x, const void* y, double* out,

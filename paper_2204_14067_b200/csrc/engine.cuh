@@ -34,14 +34,4 @@ int bcd_dispatch(int dtype, const mfg_layout* lay, int k, const void* vals, cons
 void prof_begin(cudaStream_t s);
 void prof_end(cudaStream_t s);
 
-int staged_fold(const int32_t* pptr0, const int32_t* plist0, const float* vp0, float* out0, int n0,
-                const int32_t* pptr1, const int32_t* plist1, const float* vp1, float* out1, int n1,
-                int k, int rbe, double out_scale, cudaStream_t stream);
-int staged_block_rows(int k);
-int staged_workers(int k);
-size_t staged_workspace(const mfg_staged_plan* pl);
-int staged_sweep(const mfg_staged_plan* pl, const float* W, int ldw, const float* H, int ldh,
-                 float* R, float* RH, float* RtW, double out_scale, double* sums, void* ws,
-                 size_t wsb, cudaStream_t stream);
-
 }  // namespace mfg

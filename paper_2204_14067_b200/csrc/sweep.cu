@@ -724,18 +724,24 @@ __device__ __noinline__ void finish_row(TS* out, int ldout, double out_scale, TC
   const int lane = threadIdx.x & 31;
   const int q = lane & 7;
   const unsigned gmask = 0xFFu << (lane & 24);
-  // Ordering: the group's carry stores -> warp barrier -> release fence
-  // (MEMBAR.GPU: stores acknowledged by L2, no L1 invalidation) -> counter
-  // increment. The finisher reads the pieces through L2 (ld.cg) after its
-  // own increment returned, so it observes every earlier piece. A
-  // __threadfence() here would also emit CCTL.IVALL and flush the SM's L1
-  // (the gathered factor rows) at every row crossing.
+  // Ordering (PTX memory model): every lane's carry stores -> its
+  // fence.acq_rel.gpu (run by the caller, all lanes) -> warp barrier -> the
+  // group leader's acq_rel increment of the row's arrival counter. All
+  // increments are release RMWs on one location, so the finisher's acq_rel
+  // RMW synchronises with every earlier depositor; its lanes then pass an
+  // acquire fence before reading the pieces through L2 (ld.cg). The fences
+  // are MEMBAR.GPU without the CCTL.IVALL that __threadfence() adds, so the
+  // SM's L1 (the gathered factor rows) survives a row crossing.
   int old = 0;
-  if (q == 0) old = atomicAdd(&row_cnt[frow], 1);
+  if (q == 0) {
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(row_cnt + frow) : "memory");
+  }
   old = __shfl_sync(gmask, old, lane & 24);
   const int64_t a = (int64_t)ptr[frow] / CB;
   const int64_t b = (int64_t)(ptr[frow + 1] - 1) / CB;
   if (old != (int)(b - a)) return;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   TC acc[V];
   {
     const TC* c = carry_vec + (2 * a + 1) * kp + q * V;
@@ -1034,15 +1040,14 @@ __device__ __forceinline__ double run_group(const Pass<TS, TC>& P, int chunk, in
     }
   }
   if (P.row_cnt) {
-    // Deferred crossing notification: one release fence per warp (MEMBAR.GPU,
-    // no L1 invalidation) orders all carry stores of its groups before their
-    // counter increments; the worker depositing a row's last piece finishes
-    // it. The finisher reads the pieces through L2 (ld.cg) after its own
-    // increment returned, so it observes every earlier piece.
+    // Deferred crossing notification: every lane fences its own carry
+    // stores (one MEMBAR.GPU per warp, no L1 invalidation) before the group
+    // leaders' release increments in finish_row; the worker depositing a
+    // row's last piece finishes it.
     __syncwarp();
     const bool any = __any_sync(0xffffffffu, row_first >= 0 || row_last >= 0);
     if (any) {
-      if ((threadIdx.x & 31) == 0) asm volatile("fence.release.gpu;" ::: "memory");
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       __syncwarp();
       const int64_t CB64 = CB;
       if (row_first >= 0)
@@ -1296,11 +1301,16 @@ __device__ __forceinline__ void sweep_tail(const Pass<TS, TC>& P0, const Pass<TS
     bp[3 * lblk] = b0;
     bp[3 * lblk + 1] = b1;
     bp[3 * lblk + 2] = b2;
-    asm volatile("fence.release.gpu;" ::: "memory");
-    s_last = atomicAdd(F.counter, 1u) == gridDim.x - 1;
+    // release RMW (all CTAs' increments form one release sequence); the last
+    // arriver's acq_rel RMW synchronises with every earlier block partial
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(F.counter) : "memory");
+    s_last = old == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   double u0 = 0.0, u1 = 0.0, u2 = 0.0;
   for (unsigned int b2 = threadIdx.x; b2 < gridDim.x; b2 += kGThreads) {
     u0 += __ldcg(bp + 3 * b2);

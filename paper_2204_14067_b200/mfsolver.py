@@ -79,8 +79,7 @@ class SweepPlan:
     the BASELINE metric."""
 
     def __init__(self, obs: ObservationSet, k: int, *, want_r=True, want_rh=True, want_rtw=True,
-                 out_scale: float = 1.0, compute_f64: bool = False, staged: bool = False,
-                 staged_opts: dict | None = None):
+                 out_scale: float = 1.0, compute_f64: bool = False):
         self.obs = obs
         dev = obs.dev
         dt = obs.dtype
@@ -105,18 +104,6 @@ class SweepPlan:
         self.kp = grouped_width(self.k, dt, compute_f64)
         self.ld = grouped_ld(self.k, dt, compute_f64) or self.k
         self._host = None
-        # the shared-memory staged sweep (csrc/staged.cu): fp32, k <= 64, all outputs
-        self.staged = None
-        if staged:
-            from .staged import StagedPlan
-            if dt != torch.float32 or compute_f64 or not (want_rh and want_rtw) or self.k > 64:
-                raise ValueError("the staged sweep needs fp32 storage and arithmetic, k <= 64 "
-                                 "and both R.H and R^T.W")
-            if self.ld % 4:
-                self.ld = self.kp
-            self.staged = StagedPlan(obs, self.k, want_r=want_r, **(staged_opts or {}))
-            self.wsb = self.staged.workspace_bytes()
-            self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
 
     def pad(self, f: torch.Tensor) -> torch.Tensor:
         """Factor in the grouped kernel's layout: contiguous (rows x k) when
@@ -138,12 +125,6 @@ class SweepPlan:
 
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
         """w, h: (rows x ld) with ld = k, or the zero-padded width ``kp``."""
-        if self.staged is not None:
-            _lib.check(_lib.lib().mfg_sweep_staged(
-                self.staged.ref, w.data_ptr(), int(w.stride(0)), h.data_ptr(), int(h.stride(0)),
-                _lib.ptr(self.R), self.RH.data_ptr(), self.RtW.data_ptr(), self.out_scale,
-                self.sums.data_ptr(), self.ws.data_ptr(), self.wsb, _lib.stream_ptr()), "staged sweep")
-            return
         _lib.check(_lib.lib().mfg_sweep(*self._args(w, h, _lib.stream_ptr())), "sweep")
 
     def run_host(self, w_host: torch.Tensor, h_host: torch.Tensor, *, graph: bool = True):
@@ -228,11 +209,6 @@ class SweepPlan:
         return g
 
     def _host_call(self, w_host: torch.Tensor, h_host: torch.Tensor, stream: int) -> None:
-        if self.staged is not None:
-            _lib.check(_lib.lib().mfg_sweep_staged_host(
-                self.staged.ref, w_host.data_ptr(), h_host.data_ptr(), *self._host_tail, stream),
-                "staged sweep_host")
-            return
         _lib.check(_lib.lib().mfg_sweep_host(*self._host_args, w_host.data_ptr(), h_host.data_ptr(),
                                              *self._host_tail, stream), "sweep_host")
 
@@ -277,7 +253,32 @@ def _half_sweep(obs: ObservationSet, transpose: bool, other: torch.Tensor, lam: 
     _lib.check(lib.mfg_bcd_half_sweep(_lib.dtype_code(dt), lay.ref, k, vals.data_ptr(),
                                       other.data_ptr(), k, float(lam), out.data_ptr(), k,
                                       ws.data_ptr(), wsb, _lib.stream_ptr()), "bcd half sweep")
+    if k and lay.nrows:
+        flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+        _lib.check(lib.mfg_bcd_status(ws.data_ptr(), flag.data_ptr(), _lib.stream_ptr()),
+                   "bcd status")
+        _PENDING_FLAGS.append(flag)
     return out
+
+
+_PENDING_FLAGS: list = []
+
+
+def check_bcd_status(sync: bool = True) -> None:
+    """Raise NumericalError if a half-sweep enqueued since the last check met
+    a non-SPD normal matrix (a pivot <= 0 or NaN: non-finite inputs). With
+    ``sync`` the current stream is synchronised first; without it the caller
+    must already have synchronised past the half-sweeps."""
+    if not _PENDING_FLAGS:
+        return
+    if sync:
+        torch.cuda.current_stream().synchronize()
+    bad = any(int(f[0]) != 0 for f in _PENDING_FLAGS)
+    _PENDING_FLAGS.clear()
+    if bad:
+        from .driver import NumericalError
+
+        raise NumericalError("BCD half-sweep: non-SPD normal matrix (non-finite factors or data)")
 
 
 def bcd_epoch(obs: ObservationSet, wf: FactorPair, lam: float) -> FactorPair:
@@ -290,6 +291,7 @@ def bcd_epoch(obs: ObservationSet, wf: FactorPair, lam: float) -> FactorPair:
         return wf
     w_new = _half_sweep(obs, False, wf.h, lam)
     h_new = _half_sweep(obs, True, w_new, lam)
+    check_bcd_status()
     return FactorPair(w_new, h_new)
 
 

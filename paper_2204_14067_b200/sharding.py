@@ -174,6 +174,8 @@ class ShardedMF:
         w_new = self.comm.allgather_blocks(w_loc, self.s.row_blocks)
         h_loc = self.ops.half_sweep(self.hc, w_new, lam)
         h_new = self.comm.allgather_blocks(h_loc, self.s.col_blocks)
+        if hasattr(self.ops, "check"):
+            self.ops.check()
         return w_new, h_new
 
 
@@ -201,6 +203,12 @@ class DeviceOps:
         from .mfsolver import _half_sweep
 
         return _half_sweep(obs, False, other_full, lam)
+
+    def check(self):
+        """NumericalError if a half-sweep since the last check was non-SPD."""
+        from .mfsolver import check_bcd_status
+
+        check_bcd_status()
 
     def residual(self, obs, self_rows, other_full):
         """r on the shard (fp64, the handle's CSR order): self_i . other_j - a_ij.

@@ -395,10 +395,89 @@ def gen_c1():
     print("c1", len(trace), "iters", el, "s; rank", x.rank, "F", d["obj"][-1])
 
 
+def gen_extras():
+    """rmse / rmse_factors (mfg/data.py:301-313), make_reference
+    (mfg/driver.py:464-475, with a test split) and the rank-deficient
+    _complete_basis / _prepare_block padding (mfg/eigensolver.py:53-78)."""
+    out = {}
+    rng = rng_for(4242)
+    m, n, r = 40, 50, 3
+    full = rng.standard_normal((m, r)) @ rng.standard_normal((n, r)).T
+    mask = rng.random((m, n)) < 0.5
+    test = (~mask) & (rng.random((m, n)) < 0.3)
+    rows, cols = np.nonzero(mask)
+    vals = full[rows, cols] + 0.05 * rng.standard_normal(rows.size)
+    trow, tcol = np.nonzero(test)
+    tval = full[trow, tcol] + 0.05 * rng.standard_normal(trow.size)
+    obs = rdata.ObservationSet.from_coo(m, n, rows, cols, vals)
+    split = rdata.EvalSplit(m, n, trow, tcol, tval)
+    out.update(ex_m=m, ex_n=n, ex_rows=rows, ex_cols=cols, ex_vals=vals, ex_trows=trow,
+               ex_tcols=tcol, ex_tvals=tval)
+    u, sg, v = _rand_triplet(rng, m, n, 4)
+    x = rker.SvdTriplet(u, sg, v)
+    w = rng.standard_normal((m, 5))
+    h = rng.standard_normal((n, 5))
+    out.update(ex_u=u, ex_s=sg, ex_v=v, ex_w=w, ex_h=h,
+               ex_rmse=rdata.rmse(split, x),
+               ex_rmse0=rdata.rmse(split, rker.SvdTriplet.zero(m, n)),
+               ex_rmsef=rdata.rmse_factors(split, rops.FactorPair(w, h)))
+    cfg = rdrv.SolverConfig(lam=2.0, k0=4, max_outer_iters=15, seed=11)
+    xs, metrics, tr = rdrv.make_reference(obs, split, cfg)
+    out.update(ex_ref_fstar=metrics["f_star"], ex_ref_rmse_star=metrics["rmse_star"],
+               ex_ref_rmse_zero=metrics["rmse_zero"], ex_ref_rank=xs.rank,
+               ex_ref_obj=np.array([rec.obj for rec in tr.records]),
+               ex_ref_ranks=np.array([rec.rank for rec in tr.records]),
+               ex_ref_rmse=np.array([rec.rmse for rec in tr.records]))
+    # _complete_basis: q spans e_0 and (e_1 + e_2)/sqrt(2): the next basis
+    # vectors e_0, e_1 project to zero / survive, exercising both branches
+    mq = 12
+    q = np.zeros((mq, 2))
+    q[0, 0] = 1.0
+    q[1, 1] = q[2, 1] = 1.0 / np.sqrt(2.0)
+    out.update(cb_q=q, cb_k=6, cb_out=reig._complete_basis(q, 6))
+    # _prepare_block on a rank-deficient block (rank 2 of 5 columns)
+    b = rng.standard_normal((30, 2)) @ rng.standard_normal((2, 5))
+    out.update(pb_r0=b, pb_k=5, pb_out=reig._prepare_block(b, 5))
+    try:
+        reig._complete_basis(np.eye(3)[:, :1], 4)
+    except ValueError as e:
+        out["cb_err"] = str(e)
+    np.savez_compressed(os.path.join(HERE, "extras.npz"), **out)
+    print("extras", metrics)
+
+
+def gen_c2(iters: int = 3):
+    """BASELINE configs[1] (c2) in the reference's fp64, the first ``iters``
+    outer iterations at the config's lambda; the GPU runs it in fp32 storage
+    (tests/test_c2_fp32_gpu.py: identical ranks, objectives within 1e-4)."""
+    m, n, r, c, v = synth.generate("c2")
+    m, n, r, c, v, tr = synth.canonical(m, n, r, c, v)
+    obs = rdata.ObservationSet.from_coo(m, n, r, c, v, transposed=tr)
+    kw = dict(lam=float(synth.CONFIGS["c2"].lam), k0=synth.CONFIGS["c2"].k0, seed=0,
+              max_outer_iters=iters)
+    cfg = rdrv.SolverConfig(**kw)
+    t0 = time.perf_counter()
+    x, _, trace = rdrv.solve_mf_global(obs, None, cfg)
+    el = time.perf_counter() - t0
+    d = trace_dict(trace)
+    d.update(kind="mf_global", cfg=kw, m=m, n=n, elapsed_s=el,
+             time_s=[rec.time_s for rec in trace.records],
+             numpy=np.__version__, instance="synth.generate('c2') canonical")
+    with open(os.path.join(HERE, "trace_c2.json"), "w") as fh:
+        json.dump(d, fh)
+    print("c2", len(trace), "records", el, "s; rank", x.rank, "F", d["obj"][-1])
+
+
 if __name__ == "__main__":
     print("reference", mfglobal.__version__, "numpy", np.__version__)
     if "--c1" in sys.argv:
         gen_c1()
+        sys.exit(0)
+    if "--c2" in sys.argv:
+        gen_c2()
+        sys.exit(0)
+    if "--extras" in sys.argv:
+        gen_extras()
         sys.exit(0)
     if "--estimated" in sys.argv:
         gen_traces_estimated()

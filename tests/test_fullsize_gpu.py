@@ -1,6 +1,6 @@
-"""Sweep parity at BASELINE.json's full sizes (c3: 10M entries, c4: 100M; c5
-with MFG_TEST_C5=1) through size-independent properties, since the CPU
-oracle cannot run a full c4 sweep in test time:
+"""Sweep parity at BASELINE.json's full sizes (c3: 10M entries, c4: 100M,
+c5: 253M) through size-independent properties, since the CPU oracle cannot
+run a full c4 sweep in test time:
 
 * adjointness: <R.H, W> = <R^T.W, H> = sum_e r_e (r_e + a_e) (the three
   contractions of the same residual; fp32 outputs, fp64 sums: 1e-4 rel);
@@ -21,7 +21,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-WORKLOADS = ["c3", "c4"] + (["c5"] if os.environ.get("MFG_TEST_C5") else [])
+WORKLOADS = ["c3", "c4", "c5"]
 
 
 def _fp32_sum_bound(terms, ref_row) -> float:
