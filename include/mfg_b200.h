@@ -118,12 +118,16 @@ int mfg_convert(int dtype_out, int dtype_in, int64_t count, const void* src,
  * compute_f64 != 0 forces fp64 arithmetic on f32 storage.
  * ldw/ldh >= k; padding columns must be zero. The single-launch grouped
  * kernel (row pieces finished in-kernel, last-block fp64 reductions) runs
- * when RH and RtW are both wanted and either ldw == ldh == the grouped
- * width kp (32/64 for f32, 16/32 for f64; k <= kp), or ldw == ldh == k with
- * k*sizeof(elem) a multiple of 16 (unpadded).
+ * when RH and RtW are both wanted and ldw == ldh == mfg_sweep_ld(dtype,
+ * compute_f64, k): k itself when k*sizeof(elem) is a multiple of 16
+ * (unpadded), else the grouped width kp (32/64 for f32, 16/32 for f64).
+ * Other ld take the warp-per-chunk kernel plus a deterministic epilogue.
  * The workspace must be zero-filled before its first use and not shared
  * with concurrent calls; the sweep leaves its counters zeroed.           */
 size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k);
+/* Factor row stride (elements) the single-launch sweep kernels take for
+ * width k (>= k; the columns beyond k must be zero).                     */
+int mfg_sweep_ld(int dtype, int compute_f64, int k);
 
 /* The sweep of one rank's shards: rows_csr is the CSR of
  * the rank's row block R_p (local row ids, global column ids), cols_csc the

@@ -65,6 +65,7 @@ _SIGS = {
     "mfg_gather": (_INT, [_INT, _I64, _P, _P, _P, _P]),
     "mfg_convert": (_INT, [_INT, _INT, _I64, _P, _P, _P]),
     "mfg_sweep_workspace": (_SZ, [_LP, _LP, _INT]),
+    "mfg_sweep_ld": (_INT, [_INT, _INT, _INT]),
     "mfg_sweep": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _INT, _P, _INT, _P, _P, _P, _D,
                          _P, _P, _SZ, _P]),
     "mfg_sweep_sharded": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _P, _INT, _P, _P, _INT, _P,

@@ -97,6 +97,10 @@ extern "C" int mfg_convert(int dtype_out, int dtype_in, int64_t count, const voi
   return MFG_OK;
 }
 
+extern "C" int mfg_sweep_ld(int dtype, int compute_f64, int k) {
+  return sweep_ld(dtype, compute_f64, k);
+}
+
 extern "C" size_t mfg_sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
   return sweep_workspace(csr, csc, k);
 }

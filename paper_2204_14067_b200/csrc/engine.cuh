@@ -15,6 +15,7 @@ int sweep_dispatch(int dtype, int compute_f64, const mfg_layout* csr, const mfg_
                    const void* Wg = nullptr, const void* Hg = nullptr);
 
 size_t sddmm_workspace(const mfg_layout* lay, int k);
+int sweep_ld(int dtype, int compute_f64, int k);
 int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,
                    int ldl, const double* scale, const void* Rt, int ldr, const void* A,
                    const void* G, double out_mult, void* out, double* sums, void* ws, size_t wsb,

@@ -1650,6 +1650,14 @@ size_t sweep_workspace(const mfg_layout* csr, const mfg_layout* csc, int k) {
   return s.off + 1024;
 }
 
+int sweep_ld(int dtype, int compute_f64, int k) {
+  const int es = dtype == MFG_F64 ? 8 : 4;
+  int kp = grouped_kp(k, es);
+  if (dtype != MFG_F64 && compute_f64 && kp > 32) kp = 0;
+  if (!kp) return k;
+  return (k * es) % 16 == 0 ? k : kp;
+}
+
 size_t sddmm_workspace(const mfg_layout* lay, int k) {
   Sizer s;
   carve_pass(s, lay, k, false, true);

@@ -60,14 +60,12 @@ def grouped_width(k: int, dtype, compute_f64: bool = False) -> int:
 
 
 def grouped_ld(k: int, dtype, compute_f64: bool = False) -> int:
-    """Factor row stride the grouped sweep kernel takes without padding: k
-    itself when a row is whole 16-byte chunks (k * elem % 16 == 0), else the
-    padded width kp (0 = grouped kernel not used)."""
-    kp = grouped_width(k, dtype, compute_f64)
-    if not kp:
+    """Factor row stride the single-launch grouped sweep kernel takes for
+    width k (``mfg_sweep_ld``): k itself when a row is whole 16-byte chunks
+    (k * elem % 16 == 0), else the padded width kp (0 = kernel not used)."""
+    if k < 1 or not grouped_width(k, dtype, compute_f64):
         return 0
-    elem = 4 if dtype == torch.float32 else 8
-    return k if (k * elem) % 16 == 0 else kp
+    return int(_lib.lib().mfg_sweep_ld(_lib.dtype_code(dtype), 1 if compute_f64 else 0, int(k)))
 
 
 class SweepPlan:

@@ -204,12 +204,13 @@ def test_sweep_deterministic_and_identities():
     assert lhs == pytest.approx(ra, rel=1e-4)
 
 
-@pytest.mark.parametrize("k", [3, 8, 16, 20, 30, 32, 40, 64])
+@pytest.mark.parametrize("k", [3, 8, 16, 20, 24, 30, 32, 36, 40, 44, 48, 56, 64])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("layout", ["plan", "padded"])
 def test_grouped_sweep_vs_oracle(k, dtype, layout):
     """The grouped (8-lane group) sweep kernel, with factors in the plan's
-    layout (unpadded ld = k where the kernel takes it) and zero-padded to kp."""
+    layout (mfg_sweep_ld: unpadded ld = k where the kernel takes it) and
+    zero-padded to kp; k > kp falls back to the warp-per-chunk kernel."""
     from paper_2204_14067_b200.mfsolver import SweepPlan
     m, n, r, c, v = synth.generate("c3", scale=0.03, seed=100 + k)
     m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
