@@ -752,10 +752,357 @@ int build_split(const mfg_layout* lay, Carver& c, const RowSched& rs, int grid, 
 }
 
 
+// ---------------------------------------------------------------------------
+// Warp-per-row BCD with the Gram on the fp64 tensor cores (round 2, k <= 40).
+//
+// One warp owns one row (or one segment of a heavy row) at a time and takes
+// it from a warp-granular ticket (longest first, as above), so a short row
+// costs no CTA barriers. The row's Gram G = X^T X (X = the d gathered factor
+// rows, d x k) is accumulated by mma.sync.m8n8k4.f64 (DMMA) over 8 x 8 tiles
+// of G, upper tile pairs (P <= Q) only: for 4 entries e0..e0+3 the A
+// fragment of tile P (X^T: 8 dims x 4 entries) and the B fragment of tile Q
+// (X: 4 entries x 8 dims) are the same per-lane value x[T] =
+// X[e0 + lane%4][8T + lane/4], so one gathered value per lane and tile feeds
+// every pair; the accumulators stay in registers for the whole row (k = 40:
+// 15 pairs, 30 doubles per lane). The right-hand side sum_e a_e x_e is a
+// per-lane fp64 FMA reduced over the 4 lanes of each dim in fixed order.
+// The normal matrix lam I + 2 G then goes to the warp's shared-memory slab
+// and is factored by an in-warp right-looking Cholesky; the two triangular
+// solves keep the vector in registers (lane l owns dims l, l + 32).
+// Heavy rows are cut into segments of S entries (S ~ nnz / 8192, so no
+// segment outlasts the sweep) whose packed partial Grams are summed in
+// segment order by the warp that finishes the row's last segment -- the
+// result does not depend on which warp ran which segment.
+// fp64 arithmetic throughout; per-row results are bitwise reproducible.
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kDmWarps = 4;            // warps per CTA
+constexpr int kDmMaxK = 40;            // k handled by the DMMA kernel (5 tiles)
+#ifndef MFG_BCD_DM_MINB
+#define MFG_BCD_DM_MINB 4              // CTAs per SM (128 registers)
+#endif
+
+size_t dm_smem_per_warp(int k) { return ((size_t)k * (k + 1) + k) * sizeof(double); }
+
+template <typename TS, int NT>
+__global__ void __launch_bounds__(32 * kDmWarps, MFG_BCD_DM_MINB)
+k_bcd_dm(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
+         double lam, TS* __restrict__ out, int ldout, int* __restrict__ bad,
+         const int* __restrict__ order, int* __restrict__ ticket, SplitPlan sp) {
+  constexpr int NP = NT * (NT + 1) / 2;
+  constexpr int SB = (sizeof(TS) == 4 && NT <= 3) ? 8 : 4;   // 4-entry steps per chunk
+  constexpr int CH = 4 * SB;
+  extern __shared__ __align__(16) double smw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int kl = k + 1;
+  double* G = smw + (size_t)wib * ((size_t)k * kl + k);
+  double* bv = G + (size_t)k * kl;
+  const int g = lane >> 2, tq = lane & 3;
+  const int nhr = sp.items ? sp.info[0] : 0;
+  const int nhi = sp.items ? sp.info[1] : 0;
+  const int pslot = k * (k + 1) / 2 + k;
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(ticket, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    int i, seg = 0, nseg = 1, ibase = 0, hidx = -1;
+    if (u < nhi) {
+      const int4 it = sp.items[u];
+      hidx = it.x; seg = it.y; nseg = it.z; ibase = it.w;
+      i = order[hidx];
+    } else {
+      const int t = u - nhi + nhr;
+      if (t >= lay.nrows) break;
+      i = order[t];
+    }
+    const int e0 = lay.ptr[i], e1 = lay.ptr[i + 1];
+    const int s0 = e0 + seg * sp.S;
+    const int s1 = nseg > 1 ? min(e1, s0 + sp.S) : e1;
+    double acc[NP][2];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc[p][0] = acc[p][1] = 0.0;
+    double bp[NT];
+#pragma unroll
+    for (int T = 0; T < NT; ++T) bp[T] = 0.0;
+    for (int c0 = s0; c0 < s1; c0 += CH) {
+      const int cn = min(CH, s1 - c0);
+      int colv = 0;
+      double av = 0.0;
+      if (lane < cn) {
+        colv = lay.idx[c0 + lane];
+        av = (double)vals[c0 + lane];
+      }
+      TS f[SB][NT];
+#pragma unroll
+      for (int s = 0; s < SB; ++s) {
+        const int src = 4 * s + tq;
+        const int col = __shfl_sync(0xffffffffu, colv, src & 31);
+        const TS* rowp = other + (int64_t)col * ldo;
+#pragma unroll
+        for (int T = 0; T < NT; ++T) {
+          const int d = 8 * T + g;
+          f[s][T] = (src < cn && d < k) ? rowp[d] : TS(0);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < SB; ++s) {
+        if (4 * s >= cn) break;   // warp-uniform
+        const double a = __shfl_sync(0xffffffffu, av, (4 * s + tq) & 31);
+        double x[NT];
+#pragma unroll
+        for (int T = 0; T < NT; ++T) {
+          x[T] = (double)f[s][T];
+          bp[T] = fma(a, x[T], bp[T]);
+        }
+        int pi = 0;
+#pragma unroll
+        for (int P = 0; P < NT; ++P)
+#pragma unroll
+          for (int Q = P; Q < NT; ++Q) {
+            dmma884(acc[pi][0], acc[pi][1], x[P], x[Q]);
+            ++pi;
+          }
+      }
+    }
+    // rhs: sum the 4 lanes of each dim (fixed order)
+#pragma unroll
+    for (int T = 0; T < NT; ++T) {
+      bp[T] += __shfl_xor_sync(0xffffffffu, bp[T], 1);
+      bp[T] += __shfl_xor_sync(0xffffffffu, bp[T], 2);
+    }
+    // Gram tiles -> the warp's slab (upper tiles; diagonal tiles whole)
+    {
+      int pi = 0;
+#pragma unroll
+      for (int P = 0; P < NT; ++P)
+#pragma unroll
+        for (int Q = P; Q < NT; ++Q) {
+          const int p = 8 * P + g;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = 8 * Q + 2 * tq + h;
+            if (p < k && q < k) G[p * kl + q] = acc[pi][h];
+          }
+          ++pi;
+        }
+    }
+    if (tq == 0) {
+#pragma unroll
+      for (int T = 0; T < NT; ++T)
+        if (8 * T + g < k) bv[8 * T + g] = bp[T];
+    }
+    __syncwarp();
+    if (nseg > 1) {
+      // publish this segment's packed upper Gram + rhs; the warp that
+      // deposits the row's last segment sums all of them in segment order
+      double* slot = sp.part + (size_t)u * pslot;
+      for (int x = lane; x < k * k; x += 32) {
+        const int pp = x / k, qq = x - pp * k;
+        if (qq >= pp) slot[pp * k - pp * (pp - 1) / 2 + (qq - pp)] = G[pp * kl + qq];
+      }
+      for (int x = lane; x < k; x += 32) slot[k * (k + 1) / 2 + x] = bv[x];
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      __syncwarp();
+      int old = 0;
+      if (lane == 0)
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(sp.done + hidx) : "memory");
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old != nseg - 1) continue;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (int x = lane; x < k * k; x += 32) {
+        const int pp = x / k, qq = x - pp * k;
+        if (qq < pp) continue;
+        const int off = pp * k - pp * (pp - 1) / 2 + (qq - pp);
+        double a = 0.0;
+        for (int sg = 0; sg < nseg; ++sg) a += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + off);
+        G[pp * kl + qq] = a;
+      }
+      for (int x = lane; x < k; x += 32) {
+        double a = 0.0;
+        for (int sg = 0; sg < nseg; ++sg)
+          a += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + k * (k + 1) / 2 + x);
+        bv[x] = a;
+      }
+      if (lane == 0) sp.done[hidx] = 0;   // at rest for the next call
+      __syncwarp();
+    }
+    // N = lam I + 2 G (upper), rhs = 2 b, held by lane l for dims l, l + 32
+    for (int x = lane; x < k * k; x += 32) {
+      const int p = x / k, q = x - p * k;
+      if (q >= p) G[p * kl + q] = 2.0 * G[p * kl + q] + (p == q ? lam : 0.0);
+    }
+    double y0 = lane < k ? 2.0 * bv[lane] : 0.0;
+    double y1 = lane + 32 < k ? 2.0 * bv[lane + 32] : 0.0;
+    __syncwarp();
+    // in-warp right-looking Cholesky N = U^T U (U upper, in place)
+    for (int j = 0; j < k; ++j) {
+      const double djj = G[j * kl + j];
+      if (!(djj > 0.0) && lane == 0) atomicOr(bad, 1);
+      const double ujj = sqrt(djj);
+      __syncwarp();
+      if (lane == 0) G[j * kl + j] = ujj;
+      for (int q = j + 1 + lane; q < k; q += 32) G[j * kl + q] /= ujj;
+      __syncwarp();
+      for (int q = j + 1 + lane; q < k; q += 32) {
+        const double gjq = G[j * kl + q];
+        for (int p = j + 1; p <= q; ++p) G[p * kl + q] -= G[j * kl + p] * gjq;
+      }
+      __syncwarp();
+    }
+    // U^T y = rhs (forward), then U w = y (backward); lane l owns l, l + 32
+    for (int j = 0; j < k; ++j) {
+      const double own = j < 32 ? y0 : y1;
+      double yj = __shfl_sync(0xffffffffu, own, j & 31) / G[j * kl + j];
+      if (lane == (j & 31)) { if (j < 32) y0 = yj; else y1 = yj; }
+      if (lane > j && lane < k) y0 -= G[j * kl + lane] * yj;
+      if (lane + 32 > j && lane + 32 < k) y1 -= G[j * kl + lane + 32] * yj;
+    }
+    for (int j = k - 1; j >= 0; --j) {
+      const double own = j < 32 ? y0 : y1;
+      const double wj = __shfl_sync(0xffffffffu, own, j & 31) / G[j * kl + j];
+      if (lane == (j & 31)) { if (j < 32) y0 = wj; else y1 = wj; }
+      if (lane < j) y0 -= G[lane * kl + j] * wj;
+      if (lane + 32 < j) y1 -= G[(lane + 32) * kl + j] * wj;
+    }
+    if (lane < k) out[(int64_t)i * ldout + lane] = (TS)y0;
+    if (lane + 32 < k) out[(int64_t)i * ldout + lane + 32] = (TS)y1;
+    __syncwarp();   // the slab is rewritten by the next row
+  }
+}
+
+// Warp-granular split plan: every row with more than S entries becomes
+// ceil(d / S) items (in the longest-first order, so split rows are a prefix
+// of it); items[] = (position in the order, segment, segments, first item).
+__global__ void k_seg_counts(const unsigned* __restrict__ deg, int n, int S, int* __restrict__ cnt) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    const long long d = deg[t];
+    cnt[t] = d > S ? (int)((d + S - 1) / S) : 0;
+  }
+}
+
+__global__ void k_seg_fill(const int* __restrict__ cnt, const int* __restrict__ off, int n,
+                           int4* __restrict__ items, int* __restrict__ info) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n || cnt[t] == 0) return;
+  const int base = off[t], c = cnt[t];
+  for (int sg = 0; sg < c; ++sg) items[base + sg] = make_int4(t, sg, c, base);
+  if (t + 1 == n || cnt[t + 1] == 0) {   // last split row: the prefix ends here
+    info[0] = t + 1;
+    info[1] = base + c;
+  }
+}
+
+int dm_split_len(int64_t nnz) {
+  const int64_t s = (nnz + 8191) / 8192;
+  return (int)(s < 512 ? 512 : s);
+}
+
+size_t dm_scan_temp_bytes(int n) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int*)nullptr, (int*)nullptr, n);
+  return b;
+}
+
+template <typename C>
+void take_dm_split(C& c, int64_t nnz, int n, int k, SplitPlan* sp, int** cnt, int** off,
+                   int4** items, int** info, void** tmp, size_t* tmpb) {
+  const int S = dm_split_len(nnz);
+  const size_t nitems = (size_t)(2 * (nnz / S) + 2);
+  *cnt = c.template take<int>(n > 0 ? n : 1);
+  *off = c.template take<int>(n > 0 ? n : 1);
+  *items = c.template take<int4>(nitems);
+  *info = c.template take<int>(2);
+  sp->done = c.template take<int>(nitems);
+  sp->part = c.template take<double>(nitems * (size_t)(k * (k + 1) / 2 + k));
+  *tmpb = dm_scan_temp_bytes(n > 0 ? n : 1);
+  *tmp = c.template take<char>(*tmpb);
+}
+
+int build_dm_split(const mfg_layout* lay, Carver& c, const RowSched& rs, int k, SplitPlan* sp,
+                   cudaStream_t stream) {
+  const int n = lay->nrows;
+  int *cnt, *off, *info;
+  int4* items;
+  void* tmp;
+  size_t tmpb;
+  take_dm_split(c, lay->nnz, n, k, sp, &cnt, &off, &items, &info, &tmp, &tmpb);
+  MFG_REQUIRE(c.ok, "bcd workspace too small");
+  sp->S = dm_split_len(lay->nnz);
+  const size_t nitems = (size_t)(2 * (lay->nnz / sp->S) + 2);
+  MFG_CUDA_CHECK(cudaMemsetAsync(sp->done, 0, sizeof(int) * nitems, stream));
+  MFG_CUDA_CHECK(cudaMemsetAsync(info, 0, 2 * sizeof(int), stream));
+  k_seg_counts<<<(n + 255) / 256, 256, 0, stream>>>(rs.deg, n, sp->S, cnt);
+  MFG_LAUNCH_CHECK();
+  MFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tmpb, cnt, off, n, stream));
+  k_seg_fill<<<(n + 255) / 256, 256, 0, stream>>>(cnt, off, n, items, info);
+  MFG_LAUNCH_CHECK();
+  sp->items = items;
+  sp->info = info;
+  return MFG_OK;
+}
+
+bool dm_path(int k) {
+  static const bool off = [] {
+    const char* e = getenv("MFG_BCD_NO_DMMA");
+    return e && e[0] && e[0] != '0';
+  }();
+  return !off && k >= 1 && k <= kDmMaxK;
+}
+
+template <typename TS>
+int launch_dm(const mfg_layout* lay, int k, const TS* vals, const TS* other, int ldo, double lam,
+              TS* out, int ldout, int* bad, const RowSched& rs, const SplitPlan& sp,
+              cudaStream_t stream) {
+  const size_t smem = dm_smem_per_warp(k) * kDmWarps;
+  const int nt = (k + 7) / 8;
+  int grid = (lay->nrows + kDmWarps - 1) / kDmWarps;
+  const int full = kNumSMs * MFG_BCD_DM_MINB;
+  if (grid > full) grid = full;
+  if (grid < 1) grid = 1;
+  auto go = [&](auto kern) -> int {
+    if (smem > 48 * 1024)
+      MFG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, 32 * kDmWarps, smem, stream>>>(*lay, k, vals, other, ldo, lam, out, ldout, bad,
+                                                rs.order, rs.ticket, sp);
+    MFG_LAUNCH_CHECK();
+    return MFG_OK;
+  };
+  switch (nt) {
+    case 1: return go(k_bcd_dm<TS, 1>);
+    case 2: return go(k_bcd_dm<TS, 2>);
+    case 3: return go(k_bcd_dm<TS, 3>);
+    case 4: return go(k_bcd_dm<TS, 4>);
+    case 5: return go(k_bcd_dm<TS, 5>);
+    default: break;
+  }
+  set_error("bcd: DMMA path supports k <= 40");
+  return MFG_ERR_ARG;
+}
+
 template <typename TS>
 int do_bcd(const mfg_layout* lay, int k, const void* vals, const void* other, int ldo, double lam,
            void* out, int ldout, void* ws, size_t wsb, cudaStream_t stream) {
   if (lay->nrows == 0 || k == 0) return MFG_OK;
+  if (dm_path(k)) {
+    Carver c(ws, wsb);
+    int* bad = c.take<int>(1);
+    MFG_REQUIRE(c.ok, "bcd workspace too small");
+    RowSched rs;
+    if (int st = build_sched(lay, c, &rs, stream)) return st;
+    SplitPlan sp;
+    if (int st = build_dm_split(lay, c, rs, k, &sp, stream)) return st;
+    MFG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+    return launch_dm<TS>(lay, k, (const TS*)vals, (const TS*)other, ldo, lam, (TS*)out, ldout, bad,
+                         rs, sp, stream);
+  }
   if (k > kSmemMaxK && smem_packed(k, k) <= 220 * 1024) {
     Carver c(ws, wsb);
     int* bad = c.take<int>(1);
@@ -844,6 +1191,23 @@ size_t bcd_workspace(const mfg_layout* lay, int k) {
     int4* items;
     int* info;
     take_split(s, grid_for_rows(lay->nrows), k, &sp, &items, &info);
+  }
+  if (dm_path(k) && lay) {   // the DMMA path's plan (sized on its own, after the shared prefix)
+    Sizer s2;
+    s2.take<int>(1);
+    RowSched rs2;
+    unsigned *kin2, *kout2;
+    int* rin2;
+    void* tmp2;
+    size_t tmpb2;
+    take_sched(s2, lay->nrows, &rs2, &kin2, &kout2, &rin2, &tmp2, &tmpb2);
+    SplitPlan sp;
+    int *cnt, *off, *info;
+    int4* items;
+    void* tmp;
+    size_t tmpb;
+    take_dm_split(s2, lay->nnz, lay->nrows, k, &sp, &cnt, &off, &items, &info, &tmp, &tmpb);
+    if (s2.off > s.off) s.off = s2.off;
   }
   return s.off + 512;
 }
