@@ -786,23 +786,45 @@ constexpr int kDmMaxK = 40;            // k handled by the DMMA kernel (5 tiles)
 #ifndef MFG_BCD_DM_MINB
 #define MFG_BCD_DM_MINB 4              // CTAs per SM (128 registers)
 #endif
+#ifndef MFG_BCD_DM_MINB5
+#define MFG_BCD_DM_MINB5 4             // ... for k = 33..40 (3: 168 registers, measured slower)
+#endif
 
-size_t dm_smem_per_warp(int k) { return ((size_t)k * (k + 1) + k) * sizeof(double); }
+// the warp's slab: N padded to K8 = 8 ceil(k/8) dims with row stride
+// ld = K8 (+8 when K8 % 16 == 0, so the 4 rows of a DMMA fragment load fall
+// in alternating bank halves), then the rhs
+__host__ __device__ inline int dm_ld(int k) {
+  const int k8 = 8 * ((k + 7) / 8);
+  return k8 % 16 == 8 ? k8 : k8 + 8;
+}
+size_t dm_smem_per_warp(int k) {
+  const int k8 = 8 * ((k + 7) / 8);
+  return ((size_t)k8 * dm_ld(k) + 2 * k8) * sizeof(double);
+}
+
+// CTAs per SM of an instantiation (NT = 5: 3 CTAs with 168 registers was
+// slower than 4 with 128 at c4, CSR 11.7 -> 12.4 ms, CSC 19.4 -> 22.0 ms)
+template <int NT>
+__host__ __device__ constexpr int dm_minb() { return NT >= 5 ? MFG_BCD_DM_MINB5 : MFG_BCD_DM_MINB; }
 
 template <typename TS, int NT>
-__global__ void __launch_bounds__(32 * kDmWarps, MFG_BCD_DM_MINB)
+__global__ void __launch_bounds__(32 * kDmWarps, dm_minb<NT>())
 k_bcd_dm(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
          double lam, TS* __restrict__ out, int ldout, int* __restrict__ bad,
          const int* __restrict__ order, int* __restrict__ ticket, SplitPlan sp) {
   constexpr int NP = NT * (NT + 1) / 2;
-  constexpr int SB = (sizeof(TS) == 4 && NT <= 3) ? 8 : 4;   // 4-entry steps per chunk
+  // 4-entry steps per chunk: the prefetched fragments f[SB][NT] compete with
+  // the 2 NP accumulators for registers (NT = 5: SB = 4 spilled 120 bytes)
+  constexpr int SB = NT <= 3 ? (sizeof(TS) == 4 ? 8 : 4) : (NT == 4 ? 4 : 2);
   constexpr int CH = 4 * SB;
   extern __shared__ __align__(16) double smw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int kl = k + 1;
-  double* G = smw + (size_t)wib * ((size_t)k * kl + k);
-  double* bv = G + (size_t)k * kl;
+  constexpr int K8 = 8 * NT;
+  const int kl = dm_ld(k);
+  double* G = smw + (size_t)wib * ((size_t)K8 * kl + 2 * K8);
+  double* bv = G + (size_t)K8 * kl;
+  double* rv = bv + K8;                 // 1 / U_jj
   const int g = lane >> 2, tq = lane & 3;
   const int nhr = sp.items ? sp.info[0] : 0;
   const int nhi = sp.items ? sp.info[1] : 0;
@@ -876,8 +898,12 @@ k_bcd_dm(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restric
       bp[T] += __shfl_xor_sync(0xffffffffu, bp[T], 1);
       bp[T] += __shfl_xor_sync(0xffffffffu, bp[T], 2);
     }
-    // Gram tiles -> the warp's slab (upper tiles; diagonal tiles whole)
+    // The normal matrix N = lam I + 2 G on the warp's slab, padded to K8 =
+    // 8 NT dims with an identity block (padded rhs and solution are zero).
+    // Whole rows: N (upper tiles; diagonal tiles whole) straight from the
+    // fragments. Segments of heavy rows publish the raw G instead.
     {
+      const bool whole = nseg == 1;
       int pi = 0;
 #pragma unroll
       for (int P = 0; P < NT; ++P)
@@ -887,25 +913,25 @@ k_bcd_dm(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restric
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int q = 8 * Q + 2 * tq + h;
-            if (p < k && q < k) G[p * kl + q] = acc[pi][h];
+            double v = acc[pi][h];
+            if (whole) v = 2.0 * v + (p == q ? (p < k ? lam : 1.0) : 0.0);
+            G[p * kl + q] = v;
           }
           ++pi;
         }
     }
     if (tq == 0) {
 #pragma unroll
-      for (int T = 0; T < NT; ++T)
-        if (8 * T + g < k) bv[8 * T + g] = bp[T];
+      for (int T = 0; T < NT; ++T) bv[8 * T + g] = bp[T];
     }
     __syncwarp();
     if (nseg > 1) {
       // publish this segment's packed upper Gram + rhs; the warp that
       // deposits the row's last segment sums all of them in segment order
       double* slot = sp.part + (size_t)u * pslot;
-      for (int x = lane; x < k * k; x += 32) {
-        const int pp = x / k, qq = x - pp * k;
-        if (qq >= pp) slot[pp * k - pp * (pp - 1) / 2 + (qq - pp)] = G[pp * kl + qq];
-      }
+      for (int pp = 0; pp < k; ++pp)
+        for (int qq = pp + lane; qq < k; qq += 32)
+          slot[pp * k - pp * (pp - 1) / 2 + (qq - pp)] = G[pp * kl + qq];
       for (int x = lane; x < k; x += 32) slot[k * (k + 1) / 2 + x] = bv[x];
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       __syncwarp();
@@ -916,63 +942,104 @@ k_bcd_dm(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restric
       old = __shfl_sync(0xffffffffu, old, 0);
       if (old != nseg - 1) continue;
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      for (int x = lane; x < k * k; x += 32) {
-        const int pp = x / k, qq = x - pp * k;
-        if (qq < pp) continue;
-        const int off = pp * k - pp * (pp - 1) / 2 + (qq - pp);
-        double a = 0.0;
-        for (int sg = 0; sg < nseg; ++sg) a += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + off);
-        G[pp * kl + qq] = a;
-      }
+      for (int pp = 0; pp < k; ++pp)
+        for (int qq = pp + lane; qq < k; qq += 32) {
+          const int off = pp * k - pp * (pp - 1) / 2 + (qq - pp);
+          double a = 0.0;
+          for (int sg = 0; sg < nseg; ++sg) a += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + off);
+          G[pp * kl + qq] = 2.0 * a + (pp == qq ? lam : 0.0);
+        }
       for (int x = lane; x < k; x += 32) {
         double a = 0.0;
         for (int sg = 0; sg < nseg; ++sg)
           a += __ldcg(sp.part + (size_t)(ibase + sg) * pslot + k * (k + 1) / 2 + x);
         bv[x] = a;
       }
+      for (int pp = k + lane; pp < K8; pp += 32) G[pp * kl + pp] = 1.0;   // identity padding
       if (lane == 0) sp.done[hidx] = 0;   // at rest for the next call
       __syncwarp();
     }
-    // N = lam I + 2 G (upper), rhs = 2 b, held by lane l for dims l, l + 32
-    for (int x = lane; x < k * k; x += 32) {
-      const int p = x / k, q = x - p * k;
-      if (q >= p) G[p * kl + q] = 2.0 * G[p * kl + q] + (p == q ? lam : 0.0);
-    }
-    double y0 = lane < k ? 2.0 * bv[lane] : 0.0;
-    double y1 = lane + 32 < k ? 2.0 * bv[lane + 32] : 0.0;
-    __syncwarp();
-    // in-warp right-looking Cholesky N = U^T U (U upper, in place)
-    for (int j = 0; j < k; ++j) {
-      const double djj = G[j * kl + j];
-      if (!(djj > 0.0) && lane == 0) atomicOr(bad, 1);
-      const double ujj = sqrt(djj);
-      __syncwarp();
-      if (lane == 0) G[j * kl + j] = ujj;
-      for (int q = j + 1 + lane; q < k; q += 32) G[j * kl + q] /= ujj;
-      __syncwarp();
-      for (int q = j + 1 + lane; q < k; q += 32) {
-        const double gjq = G[j * kl + q];
-        for (int p = j + 1; p <= q; ++p) G[p * kl + q] -= G[j * kl + p] * gjq;
+    // Blocked right-looking Cholesky N = U^T U in place (U upper), panels of
+    // 8 rows: the panel is factored by lanes over columns (at most 7 row
+    // updates per column), then the trailing matrix takes the panel's
+    // rank-8 update on the tensor cores (two DMMA per 8 x 8 tile pair,
+    // A = -U[panel rows][tile P], B = U[panel rows][tile Q], C = N tile).
+#pragma unroll 1
+    for (int b = 0; b < NT; ++b) {
+      const int jb = 8 * b;
+#pragma unroll 1
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = jb + jj;
+        const double djj = G[j * kl + j];
+        if (!(djj > 0.0) && lane == 0) atomicOr(bad, 1);
+        const double ujj = sqrt(djj);
+        const double rinv = 1.0 / ujj;
+        __syncwarp();
+        if (lane == 0) {
+          G[j * kl + j] = ujj;
+          rv[j] = rinv;
+        }
+        for (int q = j + 1 + lane; q < K8; q += 32) G[j * kl + q] *= rinv;
+        __syncwarp();
+        for (int q = j + 1 + lane; q < K8; q += 32) {
+          const double gjq = G[j * kl + q];
+#pragma unroll
+          for (int pp = 1; pp < 8; ++pp) {
+            const int p = j + pp;
+            if (jj + pp < 8 && p <= q) G[p * kl + q] -= G[j * kl + p] * gjq;
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      if (b + 1 < NT) {
+        double xa[NT][2];
+#pragma unroll
+        for (int P = 0; P < NT; ++P)
+          if (P > b) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s) xa[P][s] = G[(jb + 4 * s + tq) * kl + 8 * P + g];
+          }
+#pragma unroll
+        for (int P = 0; P < NT; ++P)
+#pragma unroll
+          for (int Q = 0; Q < NT; ++Q)
+            if (P > b && Q >= P) {
+              double* c = G + (8 * P + g) * kl + 8 * Q + 2 * tq;
+              double c0 = c[0], c1 = c[1];
+              dmma884(c0, c1, -xa[P][0], xa[Q][0]);
+              dmma884(c0, c1, -xa[P][1], xa[Q][1]);
+              c[0] = c0;
+              c[1] = c1;
+            }
+        __syncwarp();
+      }
     }
-    // U^T y = rhs (forward), then U w = y (backward); lane l owns l, l + 32
-    for (int j = 0; j < k; ++j) {
+    // U^T y = b (forward; lane l owns dims l, l + 32), then U w = y by rows
+    // (w_j = (y_j - U[j][j+1:] . w[j+1:]) / U_jj, a warp dot per row)
+    double y0 = lane < K8 ? 2.0 * bv[lane] : 0.0;
+    double y1 = lane + 32 < K8 ? 2.0 * bv[lane + 32] : 0.0;
+#pragma unroll 1
+    for (int j = 0; j < K8; ++j) {
       const double own = j < 32 ? y0 : y1;
-      double yj = __shfl_sync(0xffffffffu, own, j & 31) / G[j * kl + j];
+      const double yj = __shfl_sync(0xffffffffu, own, j & 31) * rv[j];
       if (lane == (j & 31)) { if (j < 32) y0 = yj; else y1 = yj; }
-      if (lane > j && lane < k) y0 -= G[j * kl + lane] * yj;
-      if (lane + 32 > j && lane + 32 < k) y1 -= G[j * kl + lane + 32] * yj;
+      if (lane > j && lane < K8) y0 -= G[j * kl + lane] * yj;
+      if (lane + 32 > j && lane + 32 < K8) y1 -= G[j * kl + lane + 32] * yj;
     }
-    for (int j = k - 1; j >= 0; --j) {
+    double w0 = 0.0, w1 = 0.0;
+#pragma unroll 1
+    for (int j = K8 - 1; j >= 0; --j) {
+      double s = 0.0;
+      if (lane > j && lane < K8) s = G[j * kl + lane] * w0;
+      if (lane + 32 > j && lane + 32 < K8) s = fma(G[j * kl + lane + 32], w1, s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       const double own = j < 32 ? y0 : y1;
-      const double wj = __shfl_sync(0xffffffffu, own, j & 31) / G[j * kl + j];
-      if (lane == (j & 31)) { if (j < 32) y0 = wj; else y1 = wj; }
-      if (lane < j) y0 -= G[lane * kl + j] * wj;
-      if (lane + 32 < j) y1 -= G[(lane + 32) * kl + j] * wj;
+      const double wj = (__shfl_sync(0xffffffffu, own, j & 31) - s) * rv[j];
+      if (lane == (j & 31)) { if (j < 32) w0 = wj; else w1 = wj; }
     }
-    if (lane < k) out[(int64_t)i * ldout + lane] = (TS)y0;
-    if (lane + 32 < k) out[(int64_t)i * ldout + lane + 32] = (TS)y1;
+    if (lane < k) out[(int64_t)i * ldout + lane] = (TS)w0;
+    if (lane + 32 < k) out[(int64_t)i * ldout + lane + 32] = (TS)w1;
     __syncwarp();   // the slab is rewritten by the next row
   }
 }
@@ -1064,7 +1131,7 @@ int launch_dm(const mfg_layout* lay, int k, const TS* vals, const TS* other, int
   const size_t smem = dm_smem_per_warp(k) * kDmWarps;
   const int nt = (k + 7) / 8;
   int grid = (lay->nrows + kDmWarps - 1) / kDmWarps;
-  const int full = kNumSMs * MFG_BCD_DM_MINB;
+  const int full = kNumSMs * (nt >= 5 ? MFG_BCD_DM_MINB5 : MFG_BCD_DM_MINB);
   if (grid > full) grid = full;
   if (grid < 1) grid = 1;
   auto go = [&](auto kern) -> int {
