@@ -210,6 +210,30 @@ int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k,
  * layer raises NumericalError (mfg/driver.py:52) for it.                   */
 int mfg_bcd_status(const void* workspace, int* flag_host, void* stream);
 
+/* ---- dense fp64 contractions of the lifting step (fp64 tensor cores) ---
+ * Row-major operands. mfg_gemm_tn: C (p x q) = alpha A^T B for tall A
+ * (m x p) and B (m x q) -- the k x k Grams of inner_product / frob_dist_sq
+ * (mfg/operators.py:67-81), H^T V and W^T U of ShiftedOperator.apply /
+ * apply_t (mfg/operators.py:102-118), the CholeskyQR Gram B^T B
+ * (orthonormalize, mfg/kernels.py:76-105), q^T S q of _ritz
+ * (mfg/eigensolver.py:81-92) and M M^T of exact_svd_short_fat
+ * (mfg/kernels.py:108-135). The contraction is split over row slices whose
+ * partials are added in slice order (bitwise reproducible); workspace from
+ * mfg_gemm_tn_workspace (0 bytes: none needed).
+ * mfg_gemm_nn: C (m x q) = alpha A (m x p) B (p x q) + beta C -- W (H^T V),
+ * the Ritz rotations q P and S q P, V = M^T U / sigma, and B R^-1.
+ * mfg_trtri_upper: X = R^-1 for an upper-triangular n x n R (the triangular
+ * solve of CholeskyQR as a product).                                     */
+size_t mfg_gemm_tn_workspace(int m, int p, int q);
+int mfg_gemm_tn(int m, int p, int q, const double* A, int lda, const double* B,
+                int ldb, double alpha, double* C, int ldc, void* workspace,
+                size_t ws_bytes, void* stream);
+int mfg_gemm_nn(int m, int p, int q, const double* A, int lda, const double* B,
+                int ldb, double alpha, double beta, double* C, int ldc,
+                void* stream);
+int mfg_trtri_upper(int n, const double* R, int ldr, double* X, int ldx,
+                    void* stream);
+
 /* ---- dense reductions ---------------------------------------------------
  * sums_host-free fp64 dot: out[0] = sum_i x_i y_i over `count` entries.    */
 int mfg_dot(int dtype, int64_t count, const void* x, const void* y,

@@ -215,6 +215,23 @@ extern "C" int mfg_bcd_half_sweep(int dtype, const mfg_layout* lay, int k, const
                       (cudaStream_t)stream);
 }
 
+extern "C" size_t mfg_gemm_tn_workspace(int m, int p, int q) { return gemm_tn_workspace(m, p, q); }
+
+extern "C" int mfg_gemm_tn(int m, int p, int q, const double* A, int lda, const double* B, int ldb,
+                           double alpha, double* C, int ldc, void* workspace, size_t ws_bytes,
+                           void* stream) {
+  return gemm_tn(m, p, q, A, lda, B, ldb, alpha, C, ldc, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int mfg_gemm_nn(int m, int p, int q, const double* A, int lda, const double* B, int ldb,
+                           double alpha, double beta, double* C, int ldc, void* stream) {
+  return gemm_nn(m, p, q, A, lda, B, ldb, alpha, beta, C, ldc, (cudaStream_t)stream);
+}
+
+extern "C" int mfg_trtri_upper(int n, const double* R, int ldr, double* X, int ldx, void* stream) {
+  return trtri_upper(n, R, ldr, X, ldx, (cudaStream_t)stream);
+}
+
 extern "C" int mfg_bcd_status(const void* workspace, int* flag_host, void* stream) {
   MFG_REQUIRE(workspace && flag_host, "null workspace or flag");
   // the half-sweep's non-SPD flag is the workspace's first word (bcd.cu do_bcd)
