@@ -51,24 +51,16 @@ class ShardComm(Comm):
         every rank)."""
         if self.world == 1:
             return t
-        t = t.contiguous()
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        import torch.distributed as dist
-
-        dist.all_gather(out, t, group=self.group)
+        out = self.gather_flat(t)
         s = out[0].clone()
-        for o in out[1:]:
-            s += o
+        for p in range(1, self.world):
+            s += out[p]
         return s
 
     def all_gather_list(self, t: torch.Tensor) -> list:
         if self.world == 1:
             return [t]
-        import torch.distributed as dist
-
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t.contiguous(), group=self.group)
-        return out
+        return list(self.gather_flat(t).unbind(0))
 
 
 class ShardedOperator:

@@ -126,7 +126,9 @@ def inner_product(ctx: _Ctx, a, b) -> float:
     lb, rb = _views(ctx, b)
     if la.shape[1] == 0 or lb.shape[1] == 0:
         return 0.0
-    return float(torch.sum(ctx.tsum(la.T @ lb) * ctx.tsum(ra.T @ rb)))
+    gl, gr = la.T @ lb, ra.T @ rb
+    both = ctx.tsum(torch.cat([gl.reshape(-1), gr.reshape(-1)]))   # one collective
+    return float(torch.sum(both[: gl.numel()] * both[gl.numel():]))
 
 
 def frob_dist_sq(ctx: _Ctx, a, b) -> float:

@@ -86,13 +86,28 @@ def make_shard(m: int, n: int, rows, cols, vals, rank: int, world: int) -> Shard
 
 
 class Comm:
-    """torch.distributed wrapper: padded all-gather of row blocks and an
-    order-deterministic fp64 sum."""
+    """torch.distributed wrapper: padded all-gather of row blocks and
+    order-deterministic fp64 sums. Every collective is one all-gather into a
+    single tensor (``ncoll`` counts them); scalar sums are batched and read
+    back with one device-to-host copy."""
 
     def __init__(self, group=None):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.ncoll = 0
+
+    def gather_flat(self, t: torch.Tensor) -> torch.Tensor:
+        """All-gather of equal-shape tensors into one (world, *t.shape) tensor."""
+        t = t.contiguous()
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.ncoll += 1
+        try:
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        except (RuntimeError, NotImplementedError, AttributeError):
+            parts = list(out.unbind(0))
+            dist.all_gather(parts, t, group=self.group)
+        return out
 
     def allgather_blocks(self, local: torch.Tensor, blocks: list) -> torch.Tensor:
         """Concatenate every rank's row block (sizes from ``blocks``)."""
@@ -102,22 +117,29 @@ class Comm:
         maxr = max(b - a for a, b in blocks)
         pad = torch.zeros((maxr, width), dtype=local.dtype, device=local.device)
         pad[: local.shape[0]] = local
-        out = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(out, pad, group=self.group)
-        return torch.cat([out[p][: b - a] for p, (a, b) in enumerate(blocks)], dim=0)
+        out = self.gather_flat(pad)
+        return torch.cat([out[p, : b - a] for p, (a, b) in enumerate(blocks)], dim=0)
+
+    def ordered_sums(self, xs, device) -> list:
+        """Rank-ordered sums of a batch of fp64 scalars (one all-gather, one
+        8*world*len(xs)-byte read-back; identical bits on every rank)."""
+        xs = [float(x) for x in xs]
+        if self.world == 1:
+            return xs
+        t = torch.tensor(xs, dtype=torch.float64, device=device)
+        g = self.gather_flat(t).cpu().numpy()
+        out = []
+        for j in range(len(xs)):
+            s = 0.0
+            for p in range(self.world):
+                s += float(g[p, j])
+            out.append(s)
+        return out
 
     def ordered_sum(self, x: float, device) -> float:
         """Sum of one fp64 scalar per rank, added in rank order (identical
         bits on every rank, independent of the collective's algorithm)."""
-        if self.world == 1:
-            return float(x)
-        t = torch.tensor([x], dtype=torch.float64, device=device)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
-        s = 0.0
-        for o in out:
-            s += float(o.item())
-        return s
+        return self.ordered_sums([x], device)[0]
 
 
 class ShardedMF:

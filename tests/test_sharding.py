@@ -52,13 +52,21 @@ def _worker(rank, world, port, out_dir):
     try:
         m, n, r, c, v, w, h = _instance()
         shard = sharding.make_shard(m, n, r, c, v, rank, world)
-        mf = sharding.ShardedMF(shard, OracleOps(), sharding.Comm(), torch.device("cpu"))
+        comm = sharding.Comm()
+        mf = sharding.ShardedMF(shard, OracleOps(), comm, torch.device("cpu"))
         W, H = torch.as_tensor(w), torch.as_tensor(h)
         rh, rtw, sq = mf.sweep(W, H)
         obj = mf.objective(W, H, 3.0)
-        w1, h1 = mf.bcd_epoch(W, H, 3.0)
+        c0 = comm.ncoll
+        w1, h1 = mf.bcd_epoch(W, H, 3.0)     # one MF-phase epoch: W / H all-gathers
+        obj1 = mf.objective(w1, h1, 3.0)     # + the guard's objective (one batched sum)
+        ncoll_epoch = comm.ncoll - c0
+        c0 = comm.ncoll
+        sums = comm.ordered_sums([rank + 0.5, 2.0 ** -rank, 1e16 * (rank + 1)], torch.device("cpu"))
+        ncoll_sums = comm.ncoll - c0
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), rh=rh.numpy(), rtw=rtw.numpy(), sq=sq,
-                 obj=obj, w1=w1.numpy(), h1=h1.numpy(),
+                 obj=obj, w1=w1.numpy(), h1=h1.numpy(), obj1=obj1, ncoll_epoch=ncoll_epoch,
+                 sums=np.array(sums), ncoll_sums=ncoll_sums,
                  rb=np.array(shard.row_block), cb=np.array(shard.col_block))
     finally:
         dist.destroy_process_group()
@@ -115,6 +123,14 @@ def test_two_ranks_gloo_match_single_process():
     # both ranks hold identical replicas and identical fp64 sums
     assert float(res[0]["sq"]) == float(res[1]["sq"])
     assert np.array_equal(res[0]["w1"], res[1]["w1"])
+    # data plane: an MF-phase epoch (BCD + objective guard) is 3 collectives,
+    # and a batch of scalars is one collective, summed in rank order
+    obj1 = orc.mf_objective(om, w1, h1, 3.0)
+    for x in res:
+        assert int(x["ncoll_epoch"]) <= 3
+        assert float(x["obj1"]) == pytest.approx(obj1, rel=1e-13)
+        assert int(x["ncoll_sums"]) == 1
+        assert list(x["sums"]) == [(0.5 + 1.5), 1.0 + 0.5, 1e16 + 2e16]
 
 
 @pytest.mark.gpu
