@@ -11,8 +11,9 @@
 //     32 x 32 = 4 x 4 DMMA tiles), rows of A/B (the contraction) streamed
 //     through shared memory 16 at a time with a register prefetch of the
 //     next chunk. The contraction is split over S row slices so that tall
-//     blocks with few tiles still fill the GPU; the S partial tiles are then
-//     added in slice order (k_fold_tn), so results are bitwise reproducible.
+//     blocks with few tiles still fill the GPU; the CTA that finishes a
+//     tile's last slice (arrival counter) adds the S partial tiles in slice
+//     order, so results are bitwise reproducible with no second launch.
 //   * k_gemm_nn: C = alpha A B + beta C, 64 x 64 tiles of C, the (short)
 //     contraction streamed 16 at a time.
 //   * k_trtri_upper: X = R^-1 for an upper-triangular R, one warp per
@@ -38,11 +39,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // C (p x q) = alpha * A^T B over rows [r0, r1) of slice blockIdx.z; S == 1
-// writes C, else the slice's partial tile goes to part[z][tile][64 x 64].
+// writes C, else the slice's partial tile goes to part[z][tile][64 x 64] and
+// the last-arriving slice of the tile (cnt[tile], zero at rest) sums them.
 __global__ void __launch_bounds__(128) k_gemm_tn(int m, int p, int q, const double* __restrict__ A,
                                                  int lda, const double* __restrict__ B, int ldb,
                                                  double alpha, double* __restrict__ C, int ldc,
-                                                 double* __restrict__ part, int S, int rps) {
+                                                 double* __restrict__ part, unsigned* __restrict__ cnt,
+                                                 int S, int rps) {
   __shared__ __align__(16) double sA[kKC][kLdW];
   __shared__ __align__(16) double sB[kKC][kLdW];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -92,9 +95,9 @@ __global__ void __launch_bounds__(128) k_gemm_tn(int m, int p, int q, const doub
     }
     __syncthreads();
   }
-  double* dst = S > 1 ? part + ((size_t)blockIdx.z * gridDim.x * gridDim.y +
-                                (size_t)blockIdx.y * gridDim.x + blockIdx.x) * kT * kT
-                      : nullptr;
+  const size_t tile = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const size_t per = (size_t)gridDim.x * gridDim.y * kT * kT;
+  double* dst = S > 1 ? part + blockIdx.z * per + tile * kT * kT : nullptr;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -108,22 +111,27 @@ __global__ void __launch_bounds__(128) k_gemm_tn(int m, int p, int q, const doub
           C[(int64_t)(p0 + lr) * ldc + q0 + lc] = alpha * acc[i][j][h];
         }
       }
-}
-
-// C = alpha * sum_z part[z] (slice order)
-__global__ void k_fold_tn(int p, int q, int S, int ntx, int nty, const double* __restrict__ part,
-                          double alpha, double* __restrict__ C, int ldc) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t per = (int64_t)ntx * nty * kT * kT;
-  if (idx >= per) return;
-  const int64_t tile = idx / (kT * kT);
-  const int e = (int)(idx - tile * kT * kT);
-  const int tx = (int)(tile % ntx), ty = (int)(tile / ntx);
-  const int r = tx * kT + e / kT, c = ty * kT + e % kT;
-  if (r >= p || c >= q) return;
-  double s = 0.0;
-  for (int z = 0; z < S; ++z) s += part[(int64_t)z * per + idx];
-  C[(int64_t)r * ldc + c] = alpha * s;
+  if (S == 1) return;
+  __shared__ int s_last;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt + tile) : "memory");
+    s_last = old == (unsigned)(S - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  for (int e = tid; e < kT * kT; e += 128) {
+    const int r = p0 + e / kT, c = q0 + e % kT;
+    if (r >= p || c >= q) continue;
+    const double* src = part + tile * kT * kT + e;
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += __ldcg(src + z * per);
+    C[(int64_t)r * ldc + c] = alpha * s;
+  }
+  if (tid == 0) cnt[tile] = 0u;   // at rest for the next call
 }
 
 // C (m x q) = alpha * A (m x p) B (p x q) + beta * C
@@ -225,10 +233,17 @@ int slices_for(int m, int ntiles) {
 
 }  // namespace
 
+// workspace: a fixed region of kMaxTiles arrival counters (zero before the
+// first use; the kernel leaves them zero -- fixed, so calls of different
+// shapes sharing one workspace never overlay partials on counters), then
+// the S partial tiles
+constexpr int kMaxTiles = 16384;
+constexpr size_t kCntBytes = (size_t)kMaxTiles * 4;
+
 size_t gemm_tn_workspace(int m, int p, int q) {
   const int ntx = (p + kT - 1) / kT, nty = (q + kT - 1) / kT;
-  const int S = slices_for(m, ntx * nty);
-  return S > 1 ? (size_t)S * ntx * nty * kT * kT * sizeof(double) : 0;
+  const int S = ntx * nty <= kMaxTiles ? slices_for(m, ntx * nty) : 1;
+  return S > 1 ? kCntBytes + (size_t)S * ntx * nty * kT * kT * sizeof(double) : 0;
 }
 
 int gemm_tn(int m, int p, int q, const double* A, int lda, const double* B, int ldb, double alpha,
@@ -241,20 +256,17 @@ int gemm_tn(int m, int p, int q, const double* A, int lda, const double* B, int 
     MFG_CUDA_CHECK(cudaMemset2DAsync(C, (size_t)ldc * 8, 0, (size_t)q * 8, p, stream));
     return MFG_OK;
   }
-  const int S = slices_for(m, ntx * nty);
+  const int S = ntx * nty <= kMaxTiles ? slices_for(m, ntx * nty) : 1;
   const int rps = (((m + S - 1) / S) + kKC - 1) / kKC * kKC;
   const int Sr = (m + rps - 1) / rps;
-  if (Sr > 1) MFG_REQUIRE(ws && wsb >= (size_t)Sr * ntx * nty * kT * kT * sizeof(double),
+  const size_t coff = kCntBytes;
+  if (Sr > 1) MFG_REQUIRE(ws && wsb >= coff + (size_t)Sr * ntx * nty * kT * kT * sizeof(double),
                           "gemm_tn workspace too small");
   dim3 grid(ntx, nty, Sr);
-  k_gemm_tn<<<grid, 128, 0, stream>>>(m, p, q, A, lda, B, ldb, alpha, C, ldc, (double*)ws, Sr, rps);
+  k_gemm_tn<<<grid, 128, 0, stream>>>(m, p, q, A, lda, B, ldb, alpha, C, ldc,
+                                      Sr > 1 ? (double*)((char*)ws + coff) : nullptr,
+                                      (unsigned*)ws, Sr, rps);
   MFG_LAUNCH_CHECK();
-  if (Sr > 1) {
-    const int64_t per = (int64_t)ntx * nty * kT * kT;
-    k_fold_tn<<<(unsigned)((per + 255) / 256), 256, 0, stream>>>(p, q, Sr, ntx, nty, (const double*)ws,
-                                                               alpha, C, ldc);
-    MFG_LAUNCH_CHECK();
-  }
   return MFG_OK;
 }
 

@@ -27,7 +27,9 @@ def _ws(nbytes: int, device) -> torch.Tensor:
     key = (device.type, device.index)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        # zero-filled: the Gram kernel's arrival counters (at the front) must
+        # start at zero; the kernel leaves them zero
+        buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         _WS[key] = buf
     return buf
 

@@ -68,7 +68,9 @@ def test_matmul_vector_and_project_out():
 @pytest.mark.parametrize("n", [1, 5, 33, 200])
 def test_triangular_inverse_and_solve(n):
     rng = np.random.default_rng(n)
-    r = np.triu(rng.standard_normal((n, n))) + 3.0 * np.eye(n)
+    # well-conditioned upper triangle (random ones are exponentially ill
+    # conditioned in n), as the CholeskyQR fast path guarantees
+    r = np.triu(0.1 * rng.standard_normal((n, n)) / np.sqrt(n)) + np.diag(1.0 + rng.random(n))
     x = dense.tri_inv_upper(_t(r)).cpu().numpy()
     assert np.allclose(np.triu(x), x)
     assert np.allclose(x @ r, np.eye(n), atol=1e-12)
@@ -89,3 +91,16 @@ def test_inner_product_on_own_grams():
     xa, xb = wa @ ha.T, wb @ hb.T
     assert P.inner_product(a, b) == pytest.approx(float(np.sum(xa * xb)), rel=1e-12)
     assert P.frob_dist_sq(a, b) == pytest.approx(float(np.sum((xa - xb) ** 2)), rel=1e-10)
+
+
+def test_gram_workspace_shared_across_shapes():
+    """Calls of different tile counts share one workspace: the arrival
+    counters live in a fixed region, so one call's partial tiles never land
+    on another call's counters (a first version placed them after
+    ntiles * 4 bytes and corrupted later calls)."""
+    torch.manual_seed(0)
+    for _ in range(2):
+        for m, p in [(1500, 762), (1500, 600), (5000, 600), (2000, 100), (1500, 762)]:
+            a = torch.randn(m, p, dtype=torch.float64, device="cuda")
+            b = torch.randn(m, p, dtype=torch.float64, device="cuda")
+            assert float((dense.gram(a, b) - a.T @ b).abs().max()) < 1e-10
