@@ -221,9 +221,7 @@ int mfg_bcd_status(const void* workspace, int* flag_host, void* stream);
  * partials are added in slice order (bitwise reproducible); workspace from
  * mfg_gemm_tn_workspace (0 bytes: none needed).
  * mfg_gemm_nn: C (m x q) = alpha A (m x p) B (p x q) + beta C -- W (H^T V),
- * the Ritz rotations q P and S q P, V = M^T U / sigma, and B R^-1.
- * mfg_trtri_upper: X = R^-1 for an upper-triangular n x n R (the triangular
- * solve of CholeskyQR as a product).                                     */
+ * the Ritz rotations q P and S q P, and V = M^T U / sigma.               */
 size_t mfg_gemm_tn_workspace(int m, int p, int q);
 int mfg_gemm_tn(int m, int p, int q, const double* A, int lda, const double* B,
                 int ldb, double alpha, double* C, int ldc, void* workspace,
@@ -231,8 +229,6 @@ int mfg_gemm_tn(int m, int p, int q, const double* A, int lda, const double* B,
 int mfg_gemm_nn(int m, int p, int q, const double* A, int lda, const double* B,
                 int ldb, double alpha, double beta, double* C, int ldc,
                 void* stream);
-int mfg_trtri_upper(int n, const double* R, int ldr, double* X, int ldx,
-                    void* stream);
 
 /* ---- dense reductions ---------------------------------------------------
  * sums_host-free fp64 dot: out[0] = sum_i x_i y_i over `count` entries.    */

@@ -83,7 +83,6 @@ _SIGS = {
     "mfg_gemm_tn_workspace": (_SZ, [_INT, _INT, _INT]),
     "mfg_gemm_tn": (_INT, [_INT, _INT, _INT, _P, _INT, _P, _INT, _D, _P, _INT, _P, _SZ, _P]),
     "mfg_gemm_nn": (_INT, [_INT, _INT, _INT, _P, _INT, _P, _INT, _D, _D, _P, _INT, _P]),
-    "mfg_trtri_upper": (_INT, [_INT, _P, _INT, _P, _INT, _P]),
     "mfg_dot": (_INT, [_INT, _I64, _P, _P, _P, _P, _SZ, _P]),
     "mfg_profile_enable": (_INT, [_INT]),
     "mfg_profile_collect": (_INT, [ctypes.POINTER(_D), ctypes.POINTER(_INT)]),

@@ -228,10 +228,6 @@ extern "C" int mfg_gemm_nn(int m, int p, int q, const double* A, int lda, const 
   return gemm_nn(m, p, q, A, lda, B, ldb, alpha, beta, C, ldc, (cudaStream_t)stream);
 }
 
-extern "C" int mfg_trtri_upper(int n, const double* R, int ldr, double* X, int ldx, void* stream) {
-  return trtri_upper(n, R, ldr, X, ldx, (cudaStream_t)stream);
-}
-
 extern "C" int mfg_bcd_status(const void* workspace, int* flag_host, void* stream) {
   MFG_REQUIRE(workspace && flag_host, "null workspace or flag");
   // the half-sweep's non-SPD flag is the workspace's first word (bcd.cu do_bcd)

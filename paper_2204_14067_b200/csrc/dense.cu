@@ -6,7 +6,7 @@
 // and the Rayleigh-Ritz projection q^T S q, mfg/kernels.py:76-105,
 // mfg/eigensolver.py:81-92; H^T V / W^T U in ShiftedOperator.apply,
 // mfg/operators.py:102-118) and tall-times-small products (W (H^T V),
-// q P, S q P, B R^-1). Both run here on mma.sync.m8n8k4.f64 (DMMA):
+// q P, S q P, M^T U / sigma). Both run here on mma.sync.m8n8k4.f64 (DMMA):
 //   * k_gemm_tn: C = alpha A^T B. 64 x 64 tiles of C per CTA (4 warps, each
 //     32 x 32 = 4 x 4 DMMA tiles), rows of A/B (the contraction) streamed
 //     through shared memory 16 at a time with a register prefetch of the
@@ -16,9 +16,6 @@
 //     order, so results are bitwise reproducible with no second launch.
 //   * k_gemm_nn: C = alpha A B + beta C, 64 x 64 tiles of C, the (short)
 //     contraction streamed 16 at a time.
-//   * k_trtri_upper: X = R^-1 for an upper-triangular R, one warp per
-//     column (back substitution with warp-reduced dots), so B R^-1 is a
-//     k_gemm_nn (CholeskyQR's triangular solve).
 // DMMA fragment conventions (PTX m8n8k4 .f64): A (8x4 row) a0 = A[lane/4][lane%4],
 // B (4x8 col) b0 = B[lane%4][lane/4], C/D (8x8) d{0,1} = D[lane/4][2(lane%4)+{0,1}].
 #include "common.cuh"
@@ -202,26 +199,6 @@ __global__ void __launch_bounds__(128) k_gemm_nn(int m, int p, int q, const doub
       }
 }
 
-// X = R^-1 (n x n, upper triangular, row-major); one warp per column j:
-// X[j][j] = 1 / R[j][j], X[i][j] = -(sum_{l=i+1..j} R[i][l] X[l][j]) / R[i][i].
-__global__ void k_trtri_upper(int n, const double* __restrict__ R, int ldr, double* __restrict__ X,
-                              int ldx) {
-  const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (j >= n) return;
-  for (int i = j + 1 + lane; i < n; i += 32) X[(int64_t)i * ldx + j] = 0.0;
-  if (lane == 0) X[(int64_t)j * ldx + j] = 1.0 / R[(int64_t)j * ldr + j];
-  __syncwarp();
-  for (int i = j - 1; i >= 0; --i) {
-    double s = 0.0;
-    for (int l = i + 1 + lane; l <= j; l += 32) s = fma(R[(int64_t)i * ldr + l], X[(int64_t)l * ldx + j], s);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) X[(int64_t)i * ldx + j] = -s / R[(int64_t)i * ldr + i];
-    __syncwarp();
-  }
-}
-
 int slices_for(int m, int ntiles) {
   // fill ~2 CTAs per SM; at least 64 contraction rows per slice
   int s = (2 * kNumSMs + ntiles - 1) / ntiles;
@@ -281,14 +258,6 @@ int gemm_nn(int m, int p, int q, const double* A, int lda, const double* B, int 
   }
   dim3 grid((m + kT - 1) / kT, (q + kT - 1) / kT);
   k_gemm_nn<<<grid, 128, 0, stream>>>(m, p, q, A, lda, B, ldb, alpha, beta, C, ldc);
-  MFG_LAUNCH_CHECK();
-  return MFG_OK;
-}
-
-int trtri_upper(int n, const double* R, int ldr, double* X, int ldx, cudaStream_t stream) {
-  MFG_REQUIRE(n >= 0 && ldr >= n && ldx >= n, "bad triangular-inverse arguments");
-  if (n == 0) return MFG_OK;
-  k_trtri_upper<<<(n + 3) / 4, 128, 0, stream>>>(n, R, ldr, X, ldx);
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }

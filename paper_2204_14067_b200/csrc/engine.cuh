@@ -21,7 +21,6 @@ int gemm_tn(int m, int p, int q, const double* A, int lda, const double* B, int 
             double* C, int ldc, void* ws, size_t wsb, cudaStream_t stream);
 int gemm_nn(int m, int p, int q, const double* A, int lda, const double* B, int ldb, double alpha,
             double beta, double* C, int ldc, cudaStream_t stream);
-int trtri_upper(int n, const double* R, int ldr, double* X, int ldx, cudaStream_t stream);
 int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,
                    int ldl, const double* scale, const void* Rt, int ldr, const void* A,
                    const void* G, double out_mult, void* out, double* sums, void* ws, size_t wsb,

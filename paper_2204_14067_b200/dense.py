@@ -9,7 +9,6 @@ mfg/proxlift.py:127-314).
 * ``matmul(a, b)``    a b     (tall a times a small b), optional
                       ``alpha``, ``beta`` and ``out``
 * ``project_out(q, x)``  x - q (q^T x)
-* ``tri_inv_upper(r)``   r^-1 for upper-triangular r (CholeskyQR's solve)
 
 Inputs are fp64 device tensors (made contiguous, 1-d vectors as columns);
 results are bitwise reproducible run to run."""
@@ -95,18 +94,3 @@ def project_out(q: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
     out = xm.clone()
     matmul(q, gram(q, xm), alpha=-1.0, beta=1.0, out=out)
     return out[:, 0] if vec else out
-
-
-def tri_inv_upper(r: torch.Tensor) -> torch.Tensor:
-    """r^-1 for an upper-triangular (n x n) r."""
-    r = _mat(r)
-    n = r.shape[0]
-    x = torch.empty((n, n), dtype=torch.float64, device=r.device)
-    _lib.check(_lib.lib().mfg_trtri_upper(n, r.data_ptr(), n, x.data_ptr(), n, _lib.stream_ptr()),
-               "trtri_upper")
-    return x
-
-
-def solve_upper_right(r: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """b r^-1 (solve x r = b for upper-triangular r)."""
-    return matmul(b, tri_inv_upper(r))
