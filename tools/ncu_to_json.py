@@ -11,7 +11,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
         "sm__cycles_elapsed.avg.per_second", "sm__cycles_active.avg", "sm__cycles_active.max",
-        "sm__cycles_elapsed.avg", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+        "sm__cycles_elapsed.avg", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
 
 rep, out = sys.argv[1], sys.argv[2]
 wl = sys.argv[3] if len(sys.argv) > 3 else None
@@ -34,7 +37,8 @@ for i, name in enumerate(h):
         if x >= 0.05:
             stalls[name[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = x
 res["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
-# derived: bytes through L2 per second against the measured LTS cap (~6300 B/cycle, B300_MICROARCH)
+# derived: bytes through L2 per second against the LTS cap (~6300 B/cycle; the round-2
+# microbenchmark tools/l2_bench.cu measured 12.75 TB/s = ~6500 B/cycle at 1.965 GHz)
 t_s = num("gpu__time_duration.sum") * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}[u[h.index("gpu__time_duration.sum")]]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 dram = num("dram__bytes_read.sum") * scale[u[h.index("dram__bytes_read.sum")]] + \
