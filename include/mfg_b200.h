@@ -166,6 +166,51 @@ int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr,
               int ldh, void* R, void* RH, void* RtW, double out_scale,
               double* sums, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- panel passes: the hot part of the sweep from shared memory --------
+ * The same arithmetic as mfg_sweep (mfg/data.py:253-263 pair_values,
+ * mfg/operators.py:108,117 the two SpMMs), for the entries whose gathered
+ * factor row is among the most frequently gathered ones: those rows are
+ * staged in shared memory in panels of mfg_panel_rows(ld) rows, and every
+ * run of a self row's entries inside one panel (a piece) is walked by an
+ * 8-lane group. The remaining (cold) entries go through mfg_sweep_sharded
+ * on their own layouts; mfg_panel_fold then adds each self row's piece
+ * outputs to the cold part in a fixed order (bitwise reproducible).
+ * fp32 storage and arithmetic; ld (= ldw = ldh) must be 32, 40 or 64.
+ * The panel layout is built by paper_2204_14067_b200/panel.py (device-side
+ * sort/scan); its arrays are documented in csrc/panel.cu.                  */
+typedef struct {
+  int32_t n_pieces;          /* pieces = output slots                        */
+  int32_t n_frows;           /* self rows that own pieces                    */
+  const int32_t* panel_ids;  /* [n_panels * mfg_panel_rows(ld)] gathered-row id, -1 = none */
+  const int32_t* pieces;     /* [n_pieces][4] {self row, first record block, length, slot},
+                                per panel by decreasing length               */
+  const int32_t* recs;       /* record blocks of 16 entries, 96 B each: 16 x u16
+                                panel-local rows, 16 x f32 A; a piece owns whole
+                                blocks; 2 blocks of padding at the end        */
+  const int32_t* frows;      /* [n_frows] self row                           */
+  const int32_t* fptr;       /* [n_frows + 1] slot range of each frow        */
+  void* r_hot;               /* out: residuals in record order, 16 per block (NULL: not wanted) */
+  void* piece_out;           /* scratch [n_pieces][ld] fp32                  */
+  void* piece_sq;            /* scratch [n_pieces] fp64 (NULL: no sum r^2)   */
+} mfg_panel_pass;
+
+/* rows of one panel for factor rows of ld floats (0: width not supported)   */
+int mfg_panel_rows(int ld);
+/* CTAs of the panel kernel (the length of cta_start)                        */
+int mfg_panel_ctas(void);
+/* Both passes' hot entries in one launch. plist: [n_list][4] {pass (0 CSR,
+ * 1 CSC), panel, first piece, end piece}, one element per panel; cta_start:
+ * [mfg_panel_ctas()] the list element each CTA starts its cyclic walk at;
+ * counters: n_list + 1 zeroed int32 (left zeroed). W, H: the factors (row
+ * stride ld).                                                              */
+int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const int32_t* cta_start,
+                    const mfg_panel_pass* csr, const mfg_panel_pass* csc, const void* W,
+                    const void* H, int32_t* counters, void* stream);
+/* out[row] += out_scale * (sum of the row's piece outputs, slot order);
+ * sums[0] += sum of piece_sq (when both are non-NULL).                     */
+int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* out, int ldout,
+                   double out_scale, double* sums, void* stream);
+
 /* ---- SDDMM with fused reductions --------------------------------------
  * p_e = sum_d L[row_e, d] * (scale ? scale[d] : 1) * Rt[col_e, d]
  * r_e = p_e - A_e (A may be NULL -> 0)

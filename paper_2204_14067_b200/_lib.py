@@ -50,6 +50,26 @@ _D = ctypes.c_double
 _SZ = ctypes.c_size_t
 _LP = ctypes.POINTER(Layout)
 
+
+class PanelPass(ctypes.Structure):
+    """mirror of ``mfg_panel_pass`` (include/mfg_b200.h)."""
+
+    _fields_ = [
+        ("n_pieces", ctypes.c_int32),
+        ("n_frows", ctypes.c_int32),
+        ("panel_ids", ctypes.c_void_p),
+        ("pieces", ctypes.c_void_p),
+        ("recs", ctypes.c_void_p),
+        ("frows", ctypes.c_void_p),
+        ("fptr", ctypes.c_void_p),
+        ("r_hot", ctypes.c_void_p),
+        ("piece_out", ctypes.c_void_p),
+        ("piece_sq", ctypes.c_void_p),
+    ]
+
+
+_PP = ctypes.POINTER(PanelPass)
+
 _SIGS = {
     "mfg_last_error": (ctypes.c_char_p, []),
     "mfg_version": (_INT, []),
@@ -72,6 +92,10 @@ _SIGS = {
                                  _P, _P, _D, _P, _P, _SZ, _P]),
     "mfg_sweep_host": (_INT, [_INT, _INT, _LP, _LP, _INT, _P, _P, _P, _P, _P, _INT, _P, _INT, _P,
                               _P, _P, _D, _P, _SZ, _P]),
+    "mfg_panel_rows": (_INT, [_INT]),
+    "mfg_panel_ctas": (_INT, []),
+    "mfg_panel_sweep": (_INT, [_INT, _INT, _P, _P, _PP, _PP, _P, _P, _P, _P]),
+    "mfg_panel_fold": (_INT, [_INT, _INT, _PP, _P, _INT, _D, _P, _P]),
     "mfg_sddmm_workspace": (_SZ, [_LP, _INT]),
     "mfg_sddmm": (_INT, [_INT, _INT, _LP, _INT, _P, _INT, _P, _P, _INT, _P, _P, _D, _P, _P, _P,
                          _SZ, _P]),

@@ -1,0 +1,469 @@
+// Panel passes of the Omega sweep: the hot part of a pass with the gathered
+// factor rows staged in shared memory.
+//
+// The sweep's two passes (CSR: r = w_i.h_j - a, R.H; CSC: the same residual,
+// R^T.W; mfg/data.py:253-263, mfg/operators.py:108,117) gather one k-wide
+// factor row per entry. With every gather served by L2 the sweep is bound by
+// the L2->SM crossbar (K4). Gather counts are Zipf-skewed, so most
+// gathers go to a few thousand rows: this file runs those entries from
+// *panels* -- sets of PR gathered rows held in one SM's shared memory (208 KB)
+// -- and leaves the remaining (cold) entries to the gather kernel in sweep.cu.
+//
+// Layout (built once per Omega and k by panel.py):
+//   panel_ids [NP][PR]   global gathered-row id of each panel slot (-1: none)
+//   pieces    [NPC]      {self row, first record block, length, output slot}:
+//                        a run of entries of one self row inside one panel, at
+//                        most Lmax entries; listed per panel by decreasing length
+//   recs                 record blocks of 16 entries (96 B): 16 x u16 panel-local
+//                        rows, then 16 x f32 A values. A piece owns whole blocks
+//                        (zero padded). Inside a piece the entries are ordered so
+//                        that the 4 entries of a batch fall into different
+//                        32-byte bank windows of the tail array where possible.
+//   plist     [NL]       {pass, panel, first piece, end piece}, one per panel
+//   cta_start [CTAs]     the list element each CTA starts at (work-proportional)
+//   frows / fptr         self rows that own pieces and their slot ranges;
+//                        slots are numbered in (self row, panel, run) order
+//
+// k_panel: persistent CTAs (one per SM) walk the panel list cyclically from
+// their start element; a CTA loads a panel that still has pieces with cp.async,
+// then its warps take rounds of 4 pieces (one per 8-lane group) from the
+// panel's global ticket, the next round's descriptors and self rows loading
+// during the current one. Records stream through a per-group cp.async ring.
+// Per 4 entries a group issues 4 conflict-free LDS.128 of the rows' first 128
+// bytes (lane q holds dims [4q, 4q+4) of 32-dim blocks), one LDS.128 of the 4
+// entries' tail chunks (k = 40: dims 32..39, lane q holds chunk q&1 of entry
+// q>>1), a transposed 8-lane butterfly that leaves entry q>>1's dot in lanes
+// 2(q>>1), 2(q>>1)+1, and the accumulation of r * row in registers. A piece
+// writes its partial output vector to its slot; k_panel_fold adds a self row's
+// slots in slot order to the cold part, so the result does not depend on which
+// CTA ran which piece (bitwise reproducible).
+#include "common.cuh"
+#include "engine.cuh"
+
+namespace mfg {
+
+namespace {
+
+constexpr int kPT = 640;               // threads per CTA (20 warps, <= 102 registers)
+constexpr int kPanelBytes = 211 * 1024; // the panel
+constexpr int kBlockBytes = 96;         // a record block: 16 x u16 local rows, 16 x f32 values
+constexpr int kRingBytes = (kPT / 32) * 4 * 2 * kBlockBytes;  // per 8-lane group: 2 blocks
+constexpr int kPanelSmem = kPanelBytes + kRingBytes;
+
+struct PanelPass {
+  const float* self;        // self rows (W in the CSR pass, H in the CSC pass)
+  const float* gath;        // gathered table
+  const int32_t* panel_ids;
+  const int4* pieces;
+  const int4* recs;         // record blocks, 6 int4 each
+  float* rhot;              // residuals in record order (nullable)
+  float* po;                // piece outputs [slot][KP]
+  double* psq;              // per-slot sum r^2 (nullable)
+  int lds, ldg;
+};
+
+struct PanelArgs {
+  PanelPass p[2];
+  const int4* plist;        // {pass, panel, first piece, end piece}
+  const int32_t* cta_start; // [gridDim.x] first list element of each CTA
+  int n_list;
+  int PR;
+  int* counters;            // [n_list] piece tickets, [n_list] finished CTAs (zero at rest)
+};
+
+__device__ __forceinline__ void cp16(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ float4 lds128(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(unsigned a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds32(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ float dot4(const float4& a, const float4& b) {
+  float2 s = __fmul2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+  s = __ffma2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w), s);
+  return s.x + s.y;
+}
+
+__device__ __forceinline__ void axpy4(float4& acc, float r, const float4& x) {
+  const float2 rr = make_float2(r, r);
+  const float2 lo = __ffma2_rn(rr, make_float2(x.x, x.y), make_float2(acc.x, acc.y));
+  const float2 hi = __ffma2_rn(rr, make_float2(x.z, x.w), make_float2(acc.z, acc.w));
+  acc.x = lo.x; acc.y = lo.y; acc.z = hi.x; acc.w = hi.y;
+}
+
+// NB: 32-dim blocks per row (k = 40: 1, k = 64: 2); KT: 16-byte tail chunks
+// (k = 40: 2; 0 when the row is whole blocks).
+template <int NB, int KT>
+__global__ void __launch_bounds__(kPT, 1) k_panel(const PanelArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int KC = NB * 8 + KT;       // 16-byte chunks per row
+  constexpr int KP = KC * 4;            // floats per row / per piece output
+  constexpr int KTD = KT > 0 ? KT : 1;
+  float* s_main = reinterpret_cast<float*>(smem_raw);
+  float* s_tail = s_main + (size_t)A.PR * NB * 32;
+  __shared__ int s_left;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 7, g = lane >> 3;
+  const int ei = q >> 1;                // the entry of a 4-batch this lane finishes
+  // this group's record ring: 2 slots of one 96-byte block (16 records = 4 batches)
+  unsigned char* ring = smem_raw + kPanelBytes + (warp * 4 + g) * 2 * kBlockBytes;
+  // 32-bit shared addresses and per-lane constants of the batch loop
+  const unsigned a_main = (unsigned)__cvta_generic_to_shared(s_main) + q * 16;
+  const unsigned a_tail = (unsigned)__cvta_generic_to_shared(s_tail) + (q % KTD) * 16;
+  const unsigned a_ring = (unsigned)__cvta_generic_to_shared(ring);
+  const bool t_hi = (ei >> 1) != 0;     // the tail entry's local row: upper word of the pair
+  const int t_sh = (ei & 1) * 16;       // ... and its half
+  const bool b2 = (q & 4) != 0, b1 = (q & 2) != 0, even = (q & 1) == 0;
+  const int gb = lane & 24;
+  int li = A.cta_start[blockIdx.x];
+  for (int step = 0; step < A.n_list; ++step, li = li + 1 == A.n_list ? 0 : li + 1) {
+    const int4 it = A.plist[li];        // {pass, panel, first piece, end piece}
+    const int npc = it.w - it.z;
+    __syncthreads();                    // everyone is done with the previous panel
+    if (tid == 0) s_left = npc - *reinterpret_cast<volatile int*>(A.counters + li);
+    __syncthreads();
+    if (s_left <= 0) continue;          // this panel's pieces are all taken
+    const PanelPass& P = A.p[it.x];
+    {
+      const int32_t* ids = P.panel_ids + (size_t)it.y * A.PR;
+      const int total = A.PR * KC;
+      for (int c = tid; c < total; c += kPT) {
+        const int r = c / KC, ch = c - r * KC;
+        const int gid = ids[r];
+        float* dst = ch < NB * 8 ? s_main + (size_t)r * NB * 32 + ch * 4
+                                 : s_tail + (size_t)r * KT * 4 + (ch - NB * 8) * 4;
+        if (gid >= 0) cp16(dst, P.gath + (size_t)gid * P.ldg + ch * 4);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_commit();
+      cp_wait<0>();
+    }
+    __syncthreads();
+    float* const rhot = P.rhot;
+    const bool st_r = rhot != nullptr && even;   // even lanes store their pair's residual
+    const bool want_sq = P.psq != nullptr;
+    // Warps take 4 consecutive pieces (one per 8-lane group) from the panel's
+    // list (sorted by decreasing length) through a global ticket, one round
+    // ahead: the next round's descriptors and self rows load during this one.
+    auto take = [&]() {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(A.counters + li, 4);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto load_desc = [&](int t0) {
+      int4 d = make_int4(0, 0, 0, -1);  // {self row, first block, length, slot}; slot < 0: none
+      if (t0 + g < npc) d = P.pieces[it.z + t0 + g];
+      return d;
+    };
+    int t_cur = take();
+    int4 pc = load_desc(t_cur);
+    float4 hm[NB], ht = make_float4(0.f, 0.f, 0.f, 0.f);
+    {
+      const float* srow = P.self + (size_t)pc.x * P.lds;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) hm[b] = *reinterpret_cast<const float4*>(srow + b * 32 + q * 4);
+      if (KT > 0) ht = *reinterpret_cast<const float4*>(srow + NB * 32 + (q % KTD) * 4);
+    }
+    while (t_cur < npc) {
+      const int t_nxt = take();
+      const int4 pcn = load_desc(t_nxt);
+      float4 hmn[NB], htn = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int len = pc.z;
+      const int lim = len - ei;         // batch b holds this lane's entry iff 4 b < lim
+      float* rh = rhot + (size_t)pc.y * 16 + ei;
+      float4 am[NB], at = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) am[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+      double sq = 0.0;
+      const int nb = (len + 3) >> 2;    // batches of 4 entries
+      const int nblk = (nb + 3) >> 2;   // record blocks of 4 batches
+      int nbw = nb;
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 8));
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 16));
+      const int nblkw = (nbw + 3) >> 2;
+      const int4* rp = P.recs + (size_t)pc.y * 6;
+      const int jmax = max(nblk - 1, 0);
+      if (q < 6) cp16(ring + q * 16, rp + q);  // block 0 -> slot 0
+      cp_commit();
+      for (int j = 0; j < nblkw; ++j) {
+        {
+          const int jn = min(j + 1, jmax);     // clamped: short pieces re-read their last block
+          if (q < 6) cp16(ring + ((j + 1) & 1) * kBlockBytes + q * 16, rp + jn * 6 + q);
+          cp_commit();
+        }
+        cp_wait<1>();
+        __syncwarp();
+        if (j == 0) {
+          // the next round's self rows (its descriptors were requested a block ago)
+          const float* srow = P.self + (size_t)pcn.x * P.lds;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) hmn[b] = *reinterpret_cast<const float4*>(srow + b * 32 + q * 4);
+          if (KT > 0) htn = *reinterpret_cast<const float4*>(srow + NB * 32 + (q % KTD) * 4);
+        }
+        const unsigned rs = a_ring + (j & 1) * kBlockBytes;
+#pragma unroll 1
+        for (int bb = 0; bb < 4; ++bb) {
+          const int b = j * 4 + bb;
+          if (b >= nbw) break;
+          // this batch's records: 4 u16 local rows, and this lane's entry's value
+          const uint2 lw = lds64(rs + bb * 8);
+          const float a_mine = lds32(rs + 32 + (bb * 4 + ei) * 4);
+          const unsigned l0 = lw.x & 0xffffu, l1 = lw.x >> 16, l2 = lw.y & 0xffffu, l3 = lw.y >> 16;
+          const unsigned lt = ((t_hi ? lw.y : lw.x) >> t_sh) & 0xffffu;
+          float4 m[4][NB];
+#pragma unroll
+          for (int x = 0; x < NB; ++x) {
+            m[0][x] = lds128(a_main + l0 * (NB * 128) + x * 128);
+            m[1][x] = lds128(a_main + l1 * (NB * 128) + x * 128);
+            m[2][x] = lds128(a_main + l2 * (NB * 128) + x * 128);
+            m[3][x] = lds128(a_main + l3 * (NB * 128) + x * 128);
+          }
+          float4 tt = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (KT > 0) tt = lds128(a_tail + lt * (KT * 16));
+          float p[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            p[i] = dot4(m[i][0], hm[0]);
+#pragma unroll
+            for (int x = 1; x < NB; ++x) p[i] += dot4(m[i][x], hm[x]);
+          }
+          // transposed butterfly over the group's 8 lanes: entry q>>1 ends in
+          // lanes 2(q>>1), 2(q>>1)+1 (fixed tree: deterministic)
+          float k0 = b2 ? p[2] : p[0], k1 = b2 ? p[3] : p[1];
+          const float s0 = b2 ? p[0] : p[2], s1 = b2 ? p[1] : p[3];
+          k0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+          k1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+          float kk = b1 ? k1 : k0;
+          const float ss = b1 ? k0 : k1;
+          kk += __shfl_xor_sync(0xffffffffu, ss, 2);
+          if (KT > 0) kk += dot4(tt, ht);
+          kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+          const bool valid = b * 4 < lim;
+          const float r = valid ? kk - a_mine : 0.f;
+          const float r0 = __shfl_sync(0xffffffffu, r, gb);
+          const float r1 = __shfl_sync(0xffffffffu, r, gb + 2);
+          const float r2 = __shfl_sync(0xffffffffu, r, gb + 4);
+          const float r3 = __shfl_sync(0xffffffffu, r, gb + 6);
+#pragma unroll
+          for (int x = 0; x < NB; ++x) {
+            axpy4(am[x], r0, m[0][x]);
+            axpy4(am[x], r1, m[1][x]);
+            axpy4(am[x], r2, m[2][x]);
+            axpy4(am[x], r3, m[3][x]);
+          }
+          if (KT > 0) axpy4(at, r, tt);
+          if (st_r && valid) rh[b * 4] = r;
+          if (want_sq) sq = fma((double)r, (double)r, sq);   // odd lanes duplicate their pair's r
+        }
+        __syncwarp();                  // slot j & 1 is refilled by the next iteration
+      }
+      cp_wait<0>();                    // drain the clamped copy before the ring is reused
+      if (nblkw == 0) {
+        const float* srow = P.self + (size_t)pcn.x * P.lds;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) hmn[b] = *reinterpret_cast<const float4*>(srow + b * 32 + q * 4);
+        if (KT > 0) htn = *reinterpret_cast<const float4*>(srow + NB * 32 + (q % KTD) * 4);
+      }
+      // the tail accumulators of lanes q = c, c+2, c+4, c+6 (entries 0..3) sum to chunk c
+      if (KT > 0) {
+#pragma unroll
+        for (int o = 2; o <= 4; o <<= 1) {
+          at.x += __shfl_xor_sync(0xffffffffu, at.x, o);
+          at.y += __shfl_xor_sync(0xffffffffu, at.y, o);
+          at.z += __shfl_xor_sync(0xffffffffu, at.z, o);
+          at.w += __shfl_xor_sync(0xffffffffu, at.w, o);
+        }
+      }
+      if (want_sq) {
+        if (!even) sq = 0.0;
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+      }
+      if (pc.w >= 0) {
+        float* o = P.po + (size_t)pc.w * KP;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) *reinterpret_cast<float4*>(o + b * 32 + q * 4) = am[b];
+        if (KT > 0 && q < KT) *reinterpret_cast<float4*>(o + NB * 32 + q * 4) = at;
+        if (want_sq && q == 0) P.psq[pc.w] = sq;
+      }
+      __syncwarp();
+      pc = pcn;
+      t_cur = t_nxt;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) hm[b] = hmn[b];
+      ht = htn;
+    }
+  }
+  // the last CTA leaves the tickets zero for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int d = atomicAdd(A.counters + A.n_list, 1);
+    if (d == (int)gridDim.x - 1) {
+      for (int i = 0; i <= A.n_list; ++i) A.counters[i] = 0;
+    }
+  }
+}
+
+// out[row] += scale * sum of the row's piece outputs, in slot order. A
+// 256-thread block takes 64 / KC self rows: 4 contiguous slot sub-ranges x
+// (row, 16-byte chunk) columns; the 4 partial sums are added in sub-range
+// order (a fixed tree), so long rows (thousands of slots) do not serialise on
+// one thread. The block after the last row block sums the per-slot r^2
+// (fixed tree) into sums[0].
+__global__ void __launch_bounds__(256)
+k_panel_fold(int n_frows, int n_row_blocks, const int32_t* __restrict__ frows,
+             const int32_t* __restrict__ fptr, const float* __restrict__ po, int KC, int k,
+             float* __restrict__ out, int ldout, float scale, const double* __restrict__ psq,
+             int n_slots, double* sums) {
+  __shared__ float4 s_part[4][64];
+  __shared__ double s_red[8];
+  if ((int)blockIdx.x < n_row_blocks) {
+    const int c = threadIdx.x & 63, sub = threadIdx.x >> 6;
+    const int rpb = 64 / KC;
+    const int rr = c / KC, ch = c - rr * KC;
+    const int f = blockIdx.x * rpb + rr;
+    const bool on = rr < rpb && f < n_frows;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (on) {
+      const int s0 = fptr[f], s1 = fptr[f + 1];
+      const int n = s1 - s0;
+      const int per = (n + 3) >> 2;
+      const int a = s0 + min(sub * per, n), b = s0 + min((sub + 1) * per, n);
+      const float4* src = reinterpret_cast<const float4*>(po) + ch;
+      int s = a;
+      for (; s + 8 <= b; s += 8) {
+        float4 t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = __ldcs(src + (size_t)(s + u) * KC);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w;
+        }
+      }
+      for (; s < b; ++s) {
+        const float4 t = __ldcs(src + (size_t)s * KC);
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+    }
+    s_part[sub][c] = acc;
+    __syncthreads();
+    if (sub == 0 && on) {
+      const float4 p0 = s_part[0][c], p1 = s_part[1][c], p2 = s_part[2][c], p3 = s_part[3][c];
+      const float tot[4] = {((p0.x + p1.x) + p2.x) + p3.x, ((p0.y + p1.y) + p2.y) + p3.y,
+                            ((p0.z + p1.z) + p2.z) + p3.z, ((p0.w + p1.w) + p2.w) + p3.w};
+      float* o = out + (size_t)frows[f] * ldout + ch * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (ch * 4 + e < k) o[e] = o[e] + scale * tot[e];
+    }
+  } else if (psq != nullptr) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n_slots; i += 256) v += psq[i];
+    const double s = block_sum<256>(v, s_red);
+    if (threadIdx.x == 0) sums[0] += s;
+  }
+}
+
+template <int NB, int KT>
+int launch_panel(const PanelArgs& A, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_panel<NB, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kPanelSmem));
+    configured = true;
+  }
+  k_panel<NB, KT><<<kNumSMs, kPT, kPanelSmem, stream>>>(A);
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}
+
+bool panel_shape(int ld, int* nb, int* kt) {
+  if (ld == 40) { *nb = 1; *kt = 2; return true; }
+  if (ld == 32) { *nb = 1; *kt = 0; return true; }
+  if (ld == 64) { *nb = 2; *kt = 0; return true; }
+  return false;
+}
+
+}  // namespace
+}  // namespace mfg
+
+using namespace mfg;
+
+extern "C" int mfg_panel_rows(int ld) {
+  int nb, kt;
+  if (!panel_shape(ld, &nb, &kt)) return 0;
+  return (kPanelBytes / ((nb * 8 + kt) * 16)) & ~1;
+}
+
+extern "C" int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const int32_t* cta_start,
+                               const mfg_panel_pass* csr, const mfg_panel_pass* csc,
+                               const void* W, const void* H, int32_t* counters, void* stream) {
+  int nb, kt;
+  MFG_REQUIRE(panel_shape(ld, &nb, &kt), "panel sweep: unsupported factor row width");
+  MFG_REQUIRE(csr && csc && plist && cta_start && counters, "panel sweep: null argument");
+  if (n_list <= 0) return MFG_OK;
+  PanelArgs A;
+  const mfg_panel_pass* pp[2] = {csr, csc};
+  for (int i = 0; i < 2; ++i) {
+    PanelPass& P = A.p[i];
+    P.self = (const float*)(i == 0 ? W : H);
+    P.gath = (const float*)(i == 0 ? H : W);
+    P.panel_ids = pp[i]->panel_ids;
+    P.pieces = (const int4*)pp[i]->pieces;
+    P.recs = (const int4*)pp[i]->recs;
+    P.rhot = (float*)pp[i]->r_hot;
+    P.po = (float*)pp[i]->piece_out;
+    P.psq = (double*)pp[i]->piece_sq;
+    P.lds = ld;
+    P.ldg = ld;
+  }
+  A.plist = (const int4*)plist;
+  A.cta_start = cta_start;
+  A.n_list = n_list;
+  A.PR = mfg_panel_rows(ld);
+  A.counters = counters;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nb == 1 && kt == 2) return launch_panel<1, 2>(A, s);
+  if (nb == 1 && kt == 0) return launch_panel<1, 0>(A, s);
+  return launch_panel<2, 0>(A, s);
+}
+
+extern "C" int mfg_panel_ctas(void) { return kNumSMs; }
+
+extern "C" int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* out, int ldout,
+                              double out_scale, double* sums, void* stream) {
+  int nb, kt;
+  MFG_REQUIRE(panel_shape(ld, &nb, &kt), "panel fold: unsupported factor row width");
+  MFG_REQUIRE(pass && out, "panel fold: null argument");
+  if (pass->n_frows <= 0) return MFG_OK;
+  const bool sq = pass->piece_sq != nullptr && sums != nullptr;
+  const int KC = nb * 8 + kt;
+  const int rpb = 64 / KC;
+  const int nrb = (pass->n_frows + rpb - 1) / rpb;
+  k_panel_fold<<<nrb + (sq ? 1 : 0), 256, 0, (cudaStream_t)stream>>>(
+      pass->n_frows, nrb, pass->frows, pass->fptr, (const float*)pass->piece_out, KC, k,
+      (float*)out, ldout, (float)out_scale, sq ? (const double*)pass->piece_sq : nullptr,
+      pass->n_pieces, sums);
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}

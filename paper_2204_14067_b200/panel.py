@@ -1,0 +1,341 @@
+"""Hybrid Omega sweep: hot entries from shared-memory panels, cold entries
+through the gather kernel (csrc/panel.cu, csrc/sweep.cu).
+
+The sweep computes R = W H^T - A on Omega, R.H, R^T.W and the fp64 sums
+(mfg/data.py:253-293, mfg/operators.py:108,117). ``HybridSweepPlan`` has the
+interface of ``mfsolver.SweepPlan`` (``run(w, h)`` -> ``R``, ``RH``, ``RtW``,
+``sums``) and splits each pass's entries once per Omega and k:
+
+* an entry is *hot* when its gathered factor row is among the most gathered
+  rows (rank < n_panels * panel_rows) and the run of its self row inside its
+  panel (a *piece*) has at least ``lmin`` entries; hot entries are reordered
+  by (panel, self row) and walked by ``k_panel`` from shared memory;
+* the remaining *cold* entries keep their order in two sub-layouts (CSR of
+  the CSR pass's cold entries, CSC of the CSC pass's) and run through the
+  grouped gather kernel (``mfg_sweep_sharded``);
+* ``mfg_panel_fold`` adds the piece outputs to the cold part in a fixed
+  order, and one gather puts R back in CSR order.
+
+The layout build below is device-side sort/scan plumbing in torch (run once
+per Omega); the arithmetic of every sweep is in libmfg_b200.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+from . import _lib
+from .data import OMEGA_PAD, ObservationSet, _LayoutBuffers, _padded
+
+
+def panel_ld(k: int, dtype) -> int:
+    """Factor row stride the panel kernel takes for width k (0: unsupported)."""
+    if dtype != torch.float32:
+        return 0
+    from .mfsolver import grouped_ld
+
+    ld = grouped_ld(int(k), dtype) or 0
+    return ld if ld and _lib.lib().mfg_panel_rows(ld) > 0 else 0
+
+
+class _PanelPass:
+    """One pass's hot layout (device arrays) + its ctypes ``mfg_panel_pass``."""
+
+    def __init__(self, lay: _LayoutBuffers, vals: torch.Tensor, n_self: int, n_gath: int, PR: int,
+                 ld: int, pass_id: int, *, lmin: int, lmax: int,
+                 max_panels: int, min_panel_entries: int, want_r: bool, want_sq: bool):
+        dev = vals.device
+        nnz = lay.nnz
+        idx = lay.idx[:nnz].long()
+        row_of = lay.row_of[:nnz].long()
+        cnt = torch.bincount(idx, minlength=n_gath)
+        order = torch.argsort(cnt, descending=True, stable=True)
+        rank = torch.empty_like(order)
+        rank[order] = torch.arange(n_gath, device=dev)
+        del cnt
+        npc = max(1, min((n_gath + PR - 1) // PR, max_panels))
+        pan_e = (rank // PR)[idx]
+        key = torch.where(pan_e < npc, pan_e, torch.full_like(pan_e, npc)).to(torch.int16)
+        del pan_e
+        skey, perm = torch.sort(key, stable=True)
+        del key
+        nh = int((skey < npc).sum().item())
+        perm = perm[:nh]
+        pkey = skey[:nh].long()
+        del skey
+        rows_s = row_of[perm]
+        k2 = pkey * n_self + rows_s
+        flag = torch.ones(nh, dtype=torch.bool, device=dev)
+        if nh > 1:
+            flag[1:] = k2[1:] != k2[:-1]
+        del k2
+        pstart = torch.nonzero(flag).flatten()
+        plen = torch.diff(pstart, append=torch.tensor([nh], device=dev))
+        ppanel = pkey[pstart]
+        keep_piece = plen >= lmin
+        ent_panel = torch.zeros(npc, dtype=torch.long, device=dev)
+        ent_panel.index_add_(0, ppanel, plen * keep_piece)
+        ok = (ent_panel >= min_panel_entries).cpu()
+        npk = npc
+        for p in range(npc):
+            if not bool(ok[p]):
+                npk = p
+                break
+        keep_piece &= ppanel < npk
+        piece_id = torch.cumsum(flag, 0) - 1
+        keep_e = keep_piece[piece_id] if nh else flag
+        del piece_id, flag
+        hot_orig = perm[keep_e]                 # original positions, (panel, row, order)
+        del perm, keep_e, pkey
+        self.n_panels = npk
+        self.n_hot = int(hot_orig.numel())
+        cold = torch.ones(nnz, dtype=torch.bool, device=dev)
+        cold[hot_orig] = False
+        self.cold_mask = cold
+        # kept pieces -> sub-pieces of at most lmax entries
+        lens = plen[keep_piece]
+        prow = rows_s[pstart][keep_piece]
+        ppan = ppanel[keep_piece]
+        del rows_s, pstart, plen, ppanel, keep_piece
+        npieces = int(lens.numel())
+        nsub = (lens + lmax - 1) // lmax
+        pid = torch.repeat_interleave(torch.arange(npieces, device=dev), nsub)
+        ns = int(pid.numel())
+        first_sub = torch.cumsum(nsub, 0) - nsub
+        j = torch.arange(ns, device=dev) - first_sub[pid]
+        base = lens[pid] // nsub[pid]
+        rem = lens[pid] % nsub[pid]
+        slen = base + (j < rem).long()
+        cstart_piece = torch.cumsum(lens, 0) - lens          # compact start of each piece
+        cstart = cstart_piece[pid] + j * base + torch.minimum(j, rem)
+        srow = prow[pid]
+        span = ppan[pid]
+        nblk = (slen + 15) // 16                             # record blocks of each sub-piece
+        bstart = torch.cumsum(nblk, 0) - nblk                # first block of each sub-piece
+        n_blocks = int(nblk.sum().item()) if ns else 0
+        self.n_blocks = n_blocks
+        # records. Inside a sub-piece the entries are ordered so that the 4
+        # entries of a batch fall into different 32-byte bank windows of the
+        # panel's tail array (window = local row mod 4) where the piece allows:
+        # the t-th entry of each window, for t = 0, 1, ...
+        sub_of_e = torch.repeat_interleave(torch.arange(ns, device=dev), slen)
+        local = rank[idx[hot_orig]] % PR
+        if self.n_hot:
+            key1 = sub_of_e * 4 + (local % 4)
+            o1 = torch.argsort(key1, stable=True)
+            k1s = key1[o1]
+            f1 = torch.ones(self.n_hot, dtype=torch.bool, device=dev)
+            f1[1:] = k1s[1:] != k1s[:-1]
+            ar = torch.arange(self.n_hot, device=dev)
+            gstart = torch.cummax(torch.where(f1, ar, torch.zeros_like(ar)), 0).values
+            key2 = sub_of_e[o1] * 2048 + (ar - gstart) * 4 + (k1s % 4)
+            del k1s, f1, gstart, key1
+            o2 = torch.argsort(key2)
+            del key2
+            o12 = o1[o2]
+            del o1, o2
+            hot_orig = hot_orig[o12]
+            local = local[o12]
+            del o12
+        ar = torch.arange(self.n_hot, device=dev)
+        ppos = bstart[sub_of_e] * 16 + (ar - cstart[sub_of_e])   # record position
+        del sub_of_e, ar
+        recs = torch.zeros((n_blocks + 2, 24), dtype=torch.int32, device=dev)
+        if self.n_hot:
+            blk, off = ppos // 16, ppos % 16
+            recs.view(torch.int16).view(n_blocks + 2, 48)[blk, off] = local.to(torch.int16)
+            recs[blk, 8 + off] = vals[:nnz][hot_orig].contiguous().view(torch.int32)
+            del blk, off
+        self.recs = recs
+        self.hot_orig = hot_orig
+        self.hot_pos = ppos
+        # panel row ids
+        ids = torch.full((max(npk, 1) * PR,), -1, dtype=torch.int32, device=dev)
+        nrows_hot = min(npk * PR, n_gath)
+        ids[:nrows_hot] = order[:nrows_hot].to(torch.int32)
+        self.panel_ids = ids
+        del rank, order, idx, row_of, local
+        # slots in (self row, panel, run) order
+        seq = torch.arange(ns, device=dev)
+        o_rs = torch.argsort(srow * max(ns, 1) + seq)
+        slot = torch.empty(ns, dtype=torch.long, device=dev)
+        slot[o_rs] = seq
+        frows, counts = torch.unique_consecutive(srow[o_rs], return_counts=True)
+        self.frows = frows.to(torch.int32)
+        fptr = torch.zeros(frows.numel() + 1, dtype=torch.int32, device=dev)
+        fptr[1:] = torch.cumsum(counts, 0).to(torch.int32)
+        self.fptr = fptr
+        # piece table: per panel by decreasing length
+        o_pl = torch.argsort(span * (lmax + 1) + (lmax - slen), stable=True)
+        pieces = torch.stack([srow[o_pl], bstart[o_pl], slen[o_pl], slot[o_pl]], dim=1).to(torch.int32)
+        self.pieces = pieces.contiguous() if ns else torch.zeros((1, 4), dtype=torch.int32, device=dev)
+        self.n_pieces = ns
+        # panel list: {pass, panel, first piece, end piece} + entries per element
+        span_s = span[o_pl]
+        if ns:
+            f3 = torch.ones(ns, dtype=torch.bool, device=dev)
+            f3[1:] = span_s[1:] != span_s[:-1]
+            ist = torch.nonzero(f3).flatten()
+            iend = torch.cat([ist[1:], torch.tensor([ns], device=dev)])
+            self.plist = torch.stack([torch.full_like(ist, pass_id), span_s[ist], ist, iend],
+                                     dim=1).to(torch.int32)
+            cum = torch.cat([torch.zeros(1, dtype=torch.long, device=dev), torch.cumsum(slen[o_pl], 0)])
+            self.plist_entries = (cum[iend] - cum[ist]).cpu()
+        else:
+            self.plist = torch.zeros((0, 4), dtype=torch.int32, device=dev)
+            self.plist_entries = torch.zeros(0, dtype=torch.long)
+        # outputs / scratch
+        self.r_hot = torch.zeros((n_blocks + 2) * 16, dtype=torch.float32, device=dev) if want_r else None
+        self.piece_out = torch.empty((max(ns, 1), ld), dtype=torch.float32, device=dev)
+        self.piece_sq = torch.zeros(max(ns, 1), dtype=torch.float64, device=dev) if want_sq else None
+        self.c = _lib.PanelPass(ns, int(self.frows.numel()), self.panel_ids.data_ptr(),
+                                self.pieces.data_ptr(), self.recs.data_ptr(),
+                                self.frows.data_ptr(), self.fptr.data_ptr(), _lib.ptr(self.r_hot),
+                                self.piece_out.data_ptr(), _lib.ptr(self.piece_sq))
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.c)
+
+
+def _cold_layout(lay: _LayoutBuffers, vals: torch.Tensor, cold: torch.Tensor):
+    """Sub-layout of the cold entries (their order kept) + their values."""
+    nnz = lay.nnz
+    dev = vals.device
+    idx = lay.idx[:nnz][cold]
+    row_of = lay.row_of[:nnz][cold]
+    nc = int(idx.numel())
+    cidx = _padded(nc, torch.int32, dev)
+    cidx.copy_(idx)
+    crow = _padded(nc, torch.int32, dev)
+    crow.copy_(row_of)
+    cvals = _padded(nc, vals.dtype, dev)
+    cvals.copy_(vals[:nnz][cold])
+    ptr = torch.zeros(lay.nrows + 1, dtype=torch.int32, device=dev)
+    if nc:
+        ptr[1:] = torch.cumsum(torch.bincount(row_of.long(), minlength=lay.nrows), 0).to(torch.int32)
+    return _LayoutBuffers(lay.nrows, lay.ncols, nc, ptr, cidx, crow), cvals
+
+
+class HybridSweepPlan:
+    """The Omega sweep with hot entries from shared-memory panels.
+
+    Same outputs as ``mfsolver.SweepPlan``: ``R`` (CSR order), ``RH``, ``RtW``
+    and ``sums`` = [sum r^2, ||W||^2, ||H||^2] (fp64). ``run(w, h)`` takes the
+    factors with row stride ``ld`` (``pad``). fp32 storage only."""
+
+    def __init__(self, obs: ObservationSet, k: int, *, want_r: bool = True, out_scale: float = 1.0,
+                 lmin: int | None = None, lmax: int | None = None,
+                 max_panels: int | None = None, min_panel_entries: int | None = None):
+        if obs.dtype != torch.float32:
+            raise ValueError("HybridSweepPlan: fp32 storage only")
+        self.obs, self.k = obs, int(k)
+        self.dt = obs.dtype
+        self.ld = panel_ld(self.k, obs.dtype)
+        if not self.ld:
+            raise ValueError(f"HybridSweepPlan: unsupported factor width k={k}")
+        env = os.environ.get
+        lmin = int(env("MFG_PANEL_LMIN", 8)) if lmin is None else lmin
+        lmax = int(env("MFG_PANEL_LMAX", 256)) if lmax is None else lmax
+        max_panels = int(env("MFG_PANEL_MAXP", 64)) if max_panels is None else max_panels
+        if min_panel_entries is None:
+            min_panel_entries = int(env("MFG_PANEL_MINE", min(400_000, max(1, obs.size // 256))))
+        lib = _lib.lib()
+        dev = obs.dev
+        self.PR = lib.mfg_panel_rows(self.ld)
+        self.out_scale = float(out_scale)
+        if lmax > 511:
+            raise ValueError("HybridSweepPlan: lmax must be <= 511")
+        kw = dict(lmin=lmin, lmax=lmax, max_panels=max_panels, min_panel_entries=min_panel_entries)
+        self.p0 = _PanelPass(dev.csr, dev.vals, obs.m, obs.n, self.PR, self.ld, 0, want_r=False,
+                             want_sq=True, **kw)
+        self.p1 = _PanelPass(dev.csc, dev.vals_csc, obs.n, obs.m, self.PR, self.ld, 1,
+                             want_r=False, want_sq=False, **kw)
+        # one list over both passes; the CSC pass's piece indices are its own
+        self.plist = torch.cat([self.p0.plist, self.p1.plist], 0).contiguous()
+        self.n_list = int(self.plist.shape[0])
+        ent = torch.cat([self.p0.plist_entries, self.p1.plist_entries]).double()
+        nctas = lib.mfg_panel_ctas()
+        if self.n_list:
+            # CTA c starts at the element holding work offset c / nctas of the total
+            edges = torch.cumsum(ent, 0)
+            at = (torch.arange(nctas, dtype=torch.float64) + 0.5) * float(edges[-1]) / nctas
+            start = torch.searchsorted(edges, at).clamp_(max=self.n_list - 1)
+        else:
+            self.plist = torch.zeros((1, 4), dtype=torch.int32, device=dev.device)
+            start = torch.zeros(nctas, dtype=torch.long)
+        self.cta_start = start.to(torch.int32).to(dev.device)
+        self.cold_csr, self.cold_vals = _cold_layout(dev.csr, dev.vals, self.p0.cold_mask)
+        self.cold_csc, self.cold_vals_csc = _cold_layout(dev.csc, dev.vals_csc, self.p1.cold_mask)
+        nnz = obs.size
+        self.want_r = want_r
+        if want_r:
+            # R in CSR order = gather from [hot residuals (padded order) | cold residuals]
+            nh_pad = (self.p0.n_blocks + 2) * 16
+            self._rcat = torch.zeros(nh_pad + self.cold_csr.nnz + OMEGA_PAD, dtype=self.dt,
+                                     device=dev.device)
+            self.p0.r_hot = self._rcat[:nh_pad]
+            self.p0.c.r_hot = self.p0.r_hot.data_ptr()
+            self._rcold = self._rcat[nh_pad:]
+            src = torch.empty(nnz, dtype=torch.int32, device=dev.device)
+            src[self.p0.hot_orig] = self.p0.hot_pos.to(torch.int32)
+            cold_pos = torch.nonzero(self.p0.cold_mask).flatten()
+            src[cold_pos] = (nh_pad + torch.arange(cold_pos.numel(), device=dev.device)).to(torch.int32)
+            self._rsrc = src
+            self.R = torch.empty(nnz, dtype=self.dt, device=dev.device)
+        else:
+            self.R = None
+        for p in (self.p0, self.p1):
+            del p.hot_orig, p.hot_pos, p.cold_mask
+        es = 4
+        nb_rh = obs.m * self.k * es
+        nb_rtw = obs.n * self.k * es
+        self._out = torch.zeros(32 + nb_rh + nb_rtw, dtype=torch.uint8, device=dev.device)
+        self.sums = self._out[:24].view(torch.float64)
+        self.RH = self._out[32:32 + nb_rh].view(self.dt).view(obs.m, self.k)
+        self.RtW = self._out[32 + nb_rh:].view(self.dt).view(obs.n, self.k)
+        self.wsb = lib.mfg_sweep_workspace(self.cold_csr.ref, self.cold_csc.ref, self.k)
+        self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
+        self.counters = torch.zeros(self.n_list + 2, dtype=torch.int32, device=dev.device)
+        self.stats = {
+            "panel_rows": self.PR, "csr_panels": self.p0.n_panels, "csc_panels": self.p1.n_panels,
+            "csr_hot": self.p0.n_hot, "csc_hot": self.p1.n_hot, "nnz": nnz,
+            "csr_pieces": self.p0.n_pieces, "csc_pieces": self.p1.n_pieces, "lmax": lmax,
+        }
+
+    def pad(self, f: torch.Tensor) -> torch.Tensor:
+        if self.ld == self.k:
+            return f.to(self.dt).contiguous()
+        out = torch.zeros((f.shape[0], self.ld), dtype=self.dt, device=self.obs.dev.device)
+        out[:, : f.shape[1]] = f
+        return out
+
+    def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
+        lib = _lib.lib()
+        st = _lib.stream_ptr()
+        if int(w.stride(0)) != self.ld or int(h.stride(0)) != self.ld:
+            raise ValueError(f"factors must have row stride {self.ld}")
+        # cold entries: grouped gather kernel; also the dense norms and the row zeroing
+        _lib.check(lib.mfg_sweep_sharded(
+            _lib.MFG_F32, 0, self.cold_csr.ref, self.cold_csc.ref, self.k,
+            self.cold_vals.data_ptr(), self.cold_vals_csc.data_ptr(),
+            w.data_ptr(), w.data_ptr(), self.ld, h.data_ptr(), h.data_ptr(), self.ld,
+            self._rcold.data_ptr() if self.want_r else None, self.RH.data_ptr(),
+            self.RtW.data_ptr(), self.out_scale, self.sums.data_ptr(), self.ws.data_ptr(),
+            self.wsb, st), "hybrid sweep (cold)")
+        if self.n_list:
+            _lib.check(lib.mfg_panel_sweep(self.ld, self.n_list, self.plist.data_ptr(),
+                                           self.cta_start.data_ptr(), self.p0.ref, self.p1.ref,
+                                           w.data_ptr(), h.data_ptr(), self.counters.data_ptr(), st),
+                       "panel sweep")
+            _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p0.ref, self.RH.data_ptr(), self.k,
+                                          self.out_scale, self.sums.data_ptr(), st), "panel fold")
+            _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p1.ref, self.RtW.data_ptr(), self.k,
+                                          self.out_scale, None, st), "panel fold")
+        if self.want_r:
+            _lib.check(lib.mfg_gather(_lib.MFG_F32, self.obs.size, self._rsrc.data_ptr(),
+                                      self._rcat.data_ptr(), self.R.data_ptr(), st), "R gather")

@@ -1,0 +1,94 @@
+"""The hybrid sweep (hot entries from shared-memory panels, csrc/panel.cu; cold
+entries through the gather kernel) against the CPU oracle's sweep
+(oracle/mfg_oracle.py: mfg/data.py:253-293, mfg/operators.py:108,117)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import mfg_oracle as orc
+from paper_2204_14067_b200 import data as D
+from paper_2204_14067_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _np(t):
+    return t.detach().double().cpu().numpy()
+
+
+def _check(plan, om, wt, ht, k):
+    plan.run(plan.pad(wt), plan.pad(ht))
+    rr, rh, rtw, sq, w2, h2 = orc.sweep(om, _np(wt), _np(ht))
+    tol = 2e-5  # fp32 storage and arithmetic against the fp64 oracle on the same fp32 inputs
+    sc = lambda a: max(1.0, np.abs(a).max())  # noqa: E731
+    assert np.max(np.abs(_np(plan.R) - rr)) <= tol * sc(rr)
+    assert np.max(np.abs(_np(plan.RH) - rh)) <= tol * 10 * sc(rh)
+    assert np.max(np.abs(_np(plan.RtW) - rtw)) <= tol * 10 * sc(rtw)
+    sums = plan.sums.cpu().numpy()
+    assert sums[0] == pytest.approx(sq, rel=tol * 10)
+    assert sums[1] == pytest.approx(w2, rel=1e-12)
+    assert sums[2] == pytest.approx(h2, rel=1e-12)
+    keep = [plan.R.clone(), plan.RH.clone(), plan.RtW.clone(), plan.sums.clone()]
+    plan.run(plan.pad(wt), plan.pad(ht))
+    for a, b in zip(keep, [plan.R, plan.RH, plan.RtW, plan.sums]):
+        assert torch.equal(a, b)  # bitwise run to run
+
+
+@pytest.mark.parametrize("k", [40, 30, 32, 64])
+@pytest.mark.parametrize("cfg", [
+    dict(),                                              # defaults
+    dict(lmin=1, lmax=5, max_panels=3),                   # short pieces, few panels
+    dict(lmin=10 ** 9),                                   # nothing hot: all entries cold
+    dict(lmin=1, max_panels=10 ** 6, min_panel_entries=1),  # every entry hot
+])
+def test_hybrid_sweep_vs_oracle(k, cfg):
+    from paper_2204_14067_b200.panel import HybridSweepPlan
+    m, n, r, c, v = synth.generate("c3", scale=0.03, seed=200 + k)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    v32 = v.astype(np.float32).astype(np.float64)
+    om = orc.from_coo(m, n, r, c, v32)
+    w, h = synth.sweep_factors(m, n, k, seed=k)
+    obs = D.ObservationSet.from_coo(m, n, r, c, v32, dtype=torch.float32)
+    wt = torch.as_tensor(w).float().cuda()
+    ht = torch.as_tensor(h).float().cuda()
+    plan = HybridSweepPlan(obs, k, **cfg)
+    if cfg.get("lmin", 0) >= 10 ** 9:
+        assert plan.stats["csr_hot"] == 0 and plan.stats["csc_hot"] == 0
+    if cfg.get("max_panels", 0) >= 10 ** 6:
+        assert plan.stats["csr_hot"] == obs.size and plan.stats["csc_hot"] == obs.size
+    _check(plan, om, wt, ht, k)
+
+
+def test_hybrid_sweep_small_and_ragged():
+    """Rows with no entries, a single entry, and a panel that is only partly filled."""
+    from paper_2204_14067_b200.panel import HybridSweepPlan
+    rng = np.random.default_rng(5)
+    m, n, k = 37, 91, 40
+    mask = rng.random((m, n)) < 0.2
+    mask[3, :] = False
+    mask[:, 7] = False
+    mask[11, :] = False
+    mask[11, 5] = True
+    r, c = np.nonzero(mask)
+    v = rng.integers(1, 6, size=len(r)).astype(np.float64)
+    om = orc.from_coo(m, n, r, c, v)
+    obs = D.ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
+    w, h = synth.sweep_factors(m, n, k, seed=3)
+    wt = torch.as_tensor(w).float().cuda()
+    ht = torch.as_tensor(h).float().cuda()
+    for cfg in (dict(lmin=1, min_panel_entries=1), dict(lmin=2, lmax=3, min_panel_entries=1)):
+        plan = HybridSweepPlan(obs, k, **cfg)
+        assert plan.stats["csr_hot"] > 0
+        _check(plan, om, wt, ht, k)
+
+
+def test_hybrid_rejects_unsupported():
+    from paper_2204_14067_b200.panel import HybridSweepPlan
+    m, n, r, c, v = synth.generate("c2", scale=0.05, seed=1)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    obs64 = D.ObservationSet.from_coo(m, n, r, c, v)
+    with pytest.raises(ValueError):
+        HybridSweepPlan(obs64, 40)
+    obs32 = obs64.with_dtype(torch.float32)
+    with pytest.raises(ValueError):
+        HybridSweepPlan(obs32, 20)
