@@ -181,6 +181,9 @@ int mfg_sweep(int dtype, int compute_f64, const mfg_layout* csr,
 typedef struct {
   int32_t n_pieces;          /* pieces = output slots                        */
   int32_t n_frows;           /* self rows that own pieces                    */
+  int32_t n_light;           /* the first n_light of them have few slots (folded
+                                by one thread per 16-byte chunk); the rest get a
+                                block each                                    */
   const int32_t* panel_ids;  /* [n_panels * mfg_panel_rows(ld)] gathered-row id, -1 = none */
   const int32_t* pieces;     /* [n_pieces][4] {self row, first record block, length, slot},
                                 per panel by decreasing length               */
@@ -188,7 +191,8 @@ typedef struct {
                                 panel-local rows, 16 x f32 A; a piece owns whole
                                 blocks; 2 blocks of padding at the end        */
   const int32_t* frows;      /* [n_frows] self row                           */
-  const int32_t* fptr;       /* [n_frows + 1] slot range of each frow        */
+  const int32_t* fbeg;       /* [n_frows] first slot of the row              */
+  const int32_t* fcnt;       /* [n_frows] number of slots of the row         */
   void* r_hot;               /* out: residuals in record order, 16 per block (NULL: not wanted) */
   void* piece_out;           /* scratch [n_pieces][ld] fp32                  */
   void* piece_sq;            /* scratch [n_pieces] fp64 (NULL: no sum r^2)   */
@@ -207,9 +211,10 @@ int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const int32_t* cta
                     const mfg_panel_pass* csr, const mfg_panel_pass* csc, const void* W,
                     const void* H, int32_t* counters, void* stream);
 /* out[row] += out_scale * (sum of the row's piece outputs, slot order);
- * sums[0] += sum of piece_sq (when both are non-NULL).                     */
+ * sums[0] += sum of piece_sq (when both are non-NULL; sq_ws: 1 KB of zeroed
+ * device scratch, left zeroed).                                            */
 int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* out, int ldout,
-                   double out_scale, double* sums, void* stream);
+                   double out_scale, double* sums, void* sq_ws, void* stream);
 
 /* ---- SDDMM with fused reductions --------------------------------------
  * p_e = sum_d L[row_e, d] * (scale ? scale[d] : 1) * Rt[col_e, d]

@@ -57,11 +57,13 @@ class PanelPass(ctypes.Structure):
     _fields_ = [
         ("n_pieces", ctypes.c_int32),
         ("n_frows", ctypes.c_int32),
+        ("n_light", ctypes.c_int32),
         ("panel_ids", ctypes.c_void_p),
         ("pieces", ctypes.c_void_p),
         ("recs", ctypes.c_void_p),
         ("frows", ctypes.c_void_p),
-        ("fptr", ctypes.c_void_p),
+        ("fbeg", ctypes.c_void_p),
+        ("fcnt", ctypes.c_void_p),
         ("r_hot", ctypes.c_void_p),
         ("piece_out", ctypes.c_void_p),
         ("piece_sq", ctypes.c_void_p),
@@ -95,7 +97,7 @@ _SIGS = {
     "mfg_panel_rows": (_INT, [_INT]),
     "mfg_panel_ctas": (_INT, []),
     "mfg_panel_sweep": (_INT, [_INT, _INT, _P, _P, _PP, _PP, _P, _P, _P, _P]),
-    "mfg_panel_fold": (_INT, [_INT, _INT, _PP, _P, _INT, _D, _P, _P]),
+    "mfg_panel_fold": (_INT, [_INT, _INT, _PP, _P, _INT, _D, _P, _P, _P]),
     "mfg_sddmm_workspace": (_SZ, [_LP, _INT]),
     "mfg_sddmm": (_INT, [_INT, _INT, _LP, _INT, _P, _INT, _P, _P, _INT, _P, _P, _D, _P, _P, _P,
                          _SZ, _P]),

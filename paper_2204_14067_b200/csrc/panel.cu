@@ -21,7 +21,7 @@
 //                        32-byte bank windows of the tail array where possible.
 //   plist     [NL]       {pass, panel, first piece, end piece}, one per panel
 //   cta_start [CTAs]     the list element each CTA starts at (work-proportional)
-//   frows / fptr         self rows that own pieces and their slot ranges;
+//   frows / fbeg / fcnt  self rows that own pieces and their slot ranges;
 //                        slots are numbered in (self row, panel, run) order
 //
 // k_panel: persistent CTAs (one per SM) walk the panel list cyclically from
@@ -324,30 +324,29 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(const PanelArgs A) {
   }
 }
 
-// out[row] += scale * sum of the row's piece outputs, in slot order. A
-// 256-thread block takes 64 / KC self rows: 4 contiguous slot sub-ranges x
-// (row, 16-byte chunk) columns; the 4 partial sums are added in sub-range
-// order (a fixed tree), so long rows (thousands of slots) do not serialise on
-// one thread. The block after the last row block sums the per-slot r^2
-// (fixed tree) into sums[0].
+// out[row] += scale * sum of the row's piece outputs, in slot order.
+// Threads are (sub-range, row, 16-byte chunk): a block takes 256 / (KC * S)
+// self rows, each row's slots cut into S contiguous sub-ranges whose partial
+// sums are added in sub-range order (a fixed tree). Light rows (few slots)
+// run with S = 1 (no shared memory, no barrier), heavy rows with one row per
+// block, so a row with thousands of slots does not serialise on one thread.
 __global__ void __launch_bounds__(256)
-k_panel_fold(int n_frows, int n_row_blocks, const int32_t* __restrict__ frows,
-             const int32_t* __restrict__ fptr, const float* __restrict__ po, int KC, int k,
-             float* __restrict__ out, int ldout, float scale, const double* __restrict__ psq,
-             int n_slots, double* sums) {
-  __shared__ float4 s_part[4][64];
-  __shared__ double s_red[8];
-  if ((int)blockIdx.x < n_row_blocks) {
-    const int c = threadIdx.x & 63, sub = threadIdx.x >> 6;
-    const int rpb = 64 / KC;
+k_panel_fold(int n_rows, int n_row_blocks, int S, const int32_t* __restrict__ frows,
+             const int32_t* __restrict__ fbeg, const int32_t* __restrict__ fcnt,
+             const float* __restrict__ po, int KC, int k, float* __restrict__ out, int ldout,
+             float scale) {
+  __shared__ float4 s_part[256];
+  {
+    const int rpb = 256 / (KC * S);
+    const int cpb = rpb * KC;
+    const int sub = threadIdx.x / cpb, c = threadIdx.x - sub * cpb;
     const int rr = c / KC, ch = c - rr * KC;
     const int f = blockIdx.x * rpb + rr;
-    const bool on = rr < rpb && f < n_frows;
+    const bool on = sub < S && f < n_rows;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (on) {
-      const int s0 = fptr[f], s1 = fptr[f + 1];
-      const int n = s1 - s0;
-      const int per = (n + 3) >> 2;
+      const int s0 = fbeg[f], n = fcnt[f];
+      const int per = (n + S - 1) / S;
       const int a = s0 + min(sub * per, n), b = s0 + min((sub + 1) * per, n);
       const float4* src = reinterpret_cast<const float4*>(po) + ch;
       int s = a;
@@ -360,27 +359,68 @@ k_panel_fold(int n_frows, int n_row_blocks, const int32_t* __restrict__ frows,
           acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w;
         }
       }
-      for (; s < b; ++s) {
-        const float4 t = __ldcs(src + (size_t)s * KC);
-        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      if (s < b) {
+        float4 t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          t[u] = s + u < b ? __ldcs(src + (size_t)(s + u) * KC) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (s + u < b) { acc.x += t[u].x; acc.y += t[u].y; acc.z += t[u].z; acc.w += t[u].w; }
+        }
       }
     }
-    s_part[sub][c] = acc;
-    __syncthreads();
-    if (sub == 0 && on) {
-      const float4 p0 = s_part[0][c], p1 = s_part[1][c], p2 = s_part[2][c], p3 = s_part[3][c];
-      const float tot[4] = {((p0.x + p1.x) + p2.x) + p3.x, ((p0.y + p1.y) + p2.y) + p3.y,
-                            ((p0.z + p1.z) + p2.z) + p3.z, ((p0.w + p1.w) + p2.w) + p3.w};
+    if (S > 1) {
+      s_part[threadIdx.x] = acc;
+      __syncthreads();
+      if (on && sub == 0) {
+        for (int u = 1; u < S; ++u) {
+          const float4 p = s_part[u * cpb + c];
+          acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+        }
+      }
+    }
+    if (on && sub == 0) {
+      const float tot[4] = {acc.x, acc.y, acc.z, acc.w};
       float* o = out + (size_t)frows[f] * ldout + ch * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (ch * 4 + e < k) o[e] = o[e] + scale * tot[e];
     }
-  } else if (psq != nullptr) {
-    double v = 0.0;
-    for (int i = threadIdx.x; i < n_slots; i += 256) v += psq[i];
-    const double s = block_sum<256>(v, s_red);
-    if (threadIdx.x == 0) sums[0] += s;
+  }
+}
+
+// sums[0] += sum of the per-slot r^2: 64 blocks over fixed contiguous chunks
+// (fixed tree inside a block), the last-arriving block adds the 64 block sums
+// in block order -- bitwise reproducible. ws: [64 doubles | arrival counter].
+constexpr int kSqBlocks = 64;
+__global__ void __launch_bounds__(256)
+k_panel_sq(int n, const double* __restrict__ psq, double* __restrict__ bp, unsigned int* counter,
+           double* sums) {
+  __shared__ double s_red[8];
+  __shared__ bool last;
+  const int per = (n + kSqBlocks - 1) / kSqBlocks;
+  const int a = min((int)blockIdx.x * per, n), b = min(a + per, n);
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  int i = a + threadIdx.x;
+  for (; i + 768 < b; i += 1024) {
+    v0 += psq[i]; v1 += psq[i + 256]; v2 += psq[i + 512]; v3 += psq[i + 768];
+  }
+  for (; i < b; i += 256) v0 += psq[i];
+  const double s = block_sum<256>((v0 + v1) + (v2 + v3), s_red);
+  if (threadIdx.x == 0) {
+    bp[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* vb = bp;
+    double t = 0.0;
+    for (int j = 0; j < kSqBlocks; ++j) t += vb[j];
+    sums[0] += t;
+    *counter = 0u;
   }
 }
 
@@ -451,19 +491,36 @@ extern "C" int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const i
 extern "C" int mfg_panel_ctas(void) { return kNumSMs; }
 
 extern "C" int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* out, int ldout,
-                              double out_scale, double* sums, void* stream) {
+                              double out_scale, double* sums, void* sq_ws, void* stream) {
   int nb, kt;
   MFG_REQUIRE(panel_shape(ld, &nb, &kt), "panel fold: unsupported factor row width");
   MFG_REQUIRE(pass && out, "panel fold: null argument");
   if (pass->n_frows <= 0) return MFG_OK;
-  const bool sq = pass->piece_sq != nullptr && sums != nullptr;
   const int KC = nb * 8 + kt;
-  const int rpb = 64 / KC;
-  const int nrb = (pass->n_frows + rpb - 1) / rpb;
-  k_panel_fold<<<nrb + (sq ? 1 : 0), 256, 0, (cudaStream_t)stream>>>(
-      pass->n_frows, nrb, pass->frows, pass->fptr, (const float*)pass->piece_out, KC, k,
-      (float*)out, ldout, (float)out_scale, sq ? (const double*)pass->piece_sq : nullptr,
-      pass->n_pieces, sums);
-  MFG_LAUNCH_CHECK();
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nl = pass->n_light, nh = pass->n_frows - pass->n_light;
+  MFG_REQUIRE(nl >= 0 && nh >= 0, "panel fold: bad light/heavy split");
+  if (nl > 0) {
+    const int rpb = 256 / KC;
+    const int nrb = (nl + rpb - 1) / rpb;
+    k_panel_fold<<<nrb, 256, 0, st>>>(nl, nrb, 1, pass->frows, pass->fbeg, pass->fcnt,
+                                      (const float*)pass->piece_out, KC, k, (float*)out, ldout,
+                                      (float)out_scale);
+    MFG_LAUNCH_CHECK();
+  }
+  if (nh > 0) {
+    const int S = 256 / KC;   // one row per block
+    k_panel_fold<<<nh, 256, 0, st>>>(nh, nh, S, pass->frows + nl, pass->fbeg + nl,
+                                     pass->fcnt + nl, (const float*)pass->piece_out, KC, k,
+                                     (float*)out, ldout, (float)out_scale);
+    MFG_LAUNCH_CHECK();
+  }
+  if (pass->piece_sq != nullptr && sums != nullptr) {
+    MFG_REQUIRE(sq_ws != nullptr, "panel fold: sum r^2 needs its workspace");
+    double* bp = (double*)sq_ws;
+    k_panel_sq<<<kSqBlocks, 256, 0, st>>>(pass->n_pieces, (const double*)pass->piece_sq, bp,
+                                          (unsigned int*)(bp + kSqBlocks), sums);
+    MFG_LAUNCH_CHECK();
+  }
   return MFG_OK;
 }

@@ -165,10 +165,13 @@ class _PanelPass:
         slot = torch.empty(ns, dtype=torch.long, device=dev)
         slot[o_rs] = seq
         frows, counts = torch.unique_consecutive(srow[o_rs], return_counts=True)
-        self.frows = frows.to(torch.int32)
-        fptr = torch.zeros(frows.numel() + 1, dtype=torch.int32, device=dev)
-        fptr[1:] = torch.cumsum(counts, 0).to(torch.int32)
-        self.fptr = fptr
+        fbeg = torch.cumsum(counts, 0) - counts
+        # light rows (<= 32 slots) first, heavy rows after them
+        o_lh = torch.argsort((counts > 32).to(torch.int8), stable=True)
+        self.n_light = int((counts <= 32).sum().item()) if ns else 0
+        self.frows = frows[o_lh].to(torch.int32)
+        self.fbeg = fbeg[o_lh].to(torch.int32)
+        self.fcnt = counts[o_lh].to(torch.int32)
         # piece table: per panel by decreasing length
         o_pl = torch.argsort(span * (lmax + 1) + (lmax - slen), stable=True)
         pieces = torch.stack([srow[o_pl], bstart[o_pl], slen[o_pl], slot[o_pl]], dim=1).to(torch.int32)
@@ -192,9 +195,10 @@ class _PanelPass:
         self.r_hot = torch.zeros((n_blocks + 2) * 16, dtype=torch.float32, device=dev) if want_r else None
         self.piece_out = torch.empty((max(ns, 1), ld), dtype=torch.float32, device=dev)
         self.piece_sq = torch.zeros(max(ns, 1), dtype=torch.float64, device=dev) if want_sq else None
-        self.c = _lib.PanelPass(ns, int(self.frows.numel()), self.panel_ids.data_ptr(),
+        self.c = _lib.PanelPass(ns, int(self.frows.numel()), self.n_light, self.panel_ids.data_ptr(),
                                 self.pieces.data_ptr(), self.recs.data_ptr(),
-                                self.frows.data_ptr(), self.fptr.data_ptr(), _lib.ptr(self.r_hot),
+                                self.frows.data_ptr(), self.fbeg.data_ptr(), self.fcnt.data_ptr(),
+                                _lib.ptr(self.r_hot),
                                 self.piece_out.data_ptr(), _lib.ptr(self.piece_sq))
 
     @property
@@ -243,7 +247,7 @@ class HybridSweepPlan:
         lmax = int(env("MFG_PANEL_LMAX", 256)) if lmax is None else lmax
         max_panels = int(env("MFG_PANEL_MAXP", 64)) if max_panels is None else max_panels
         if min_panel_entries is None:
-            min_panel_entries = int(env("MFG_PANEL_MINE", min(400_000, max(1, obs.size // 256))))
+            min_panel_entries = int(env("MFG_PANEL_MINE", min(100_000, max(1, obs.size // 256))))
         lib = _lib.lib()
         dev = obs.dev
         self.PR = lib.mfg_panel_rows(self.ld)
@@ -301,6 +305,7 @@ class HybridSweepPlan:
         self.wsb = lib.mfg_sweep_workspace(self.cold_csr.ref, self.cold_csc.ref, self.k)
         self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
         self.counters = torch.zeros(self.n_list + 2, dtype=torch.int32, device=dev.device)
+        self.sq_ws = torch.zeros(1024, dtype=torch.uint8, device=dev.device)
         self.stats = {
             "panel_rows": self.PR, "csr_panels": self.p0.n_panels, "csc_panels": self.p1.n_panels,
             "csr_hot": self.p0.n_hot, "csc_hot": self.p1.n_hot, "nnz": nnz,
@@ -333,9 +338,10 @@ class HybridSweepPlan:
                                            w.data_ptr(), h.data_ptr(), self.counters.data_ptr(), st),
                        "panel sweep")
             _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p0.ref, self.RH.data_ptr(), self.k,
-                                          self.out_scale, self.sums.data_ptr(), st), "panel fold")
+                                          self.out_scale, self.sums.data_ptr(), self.sq_ws.data_ptr(), st),
+                       "panel fold")
             _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p1.ref, self.RtW.data_ptr(), self.k,
-                                          self.out_scale, None, st), "panel fold")
+                                          self.out_scale, None, None, st), "panel fold")
         if self.want_r:
             _lib.check(lib.mfg_gather(_lib.MFG_F32, self.obs.size, self._rsrc.data_ptr(),
                                       self._rcat.data_ptr(), self.R.data_ptr(), st), "R gather")

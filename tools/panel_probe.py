@@ -105,8 +105,8 @@ def pan():
 
 
 def fold():
-    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p0.ref, hyb.RH.data_ptr(), k, 1.0, hyb.sums.data_ptr(), st), "f")
-    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p1.ref, hyb.RtW.data_ptr(), k, 1.0, None, st), "f")
+    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p0.ref, hyb.RH.data_ptr(), k, 1.0, hyb.sums.data_ptr(), hyb.sq_ws.data_ptr(), st), "f")
+    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p1.ref, hyb.RtW.data_ptr(), k, 1.0, None, None, st), "f")
 
 
 def rg():
