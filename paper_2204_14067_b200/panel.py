@@ -319,6 +319,73 @@ class HybridSweepPlan:
         out[:, : f.shape[1]] = f
         return out
 
+    kind = "hybrid"
+
+    # ---- end to end from host factors (the interface of SweepPlan.run_host) ----
+    def pinned_factors(self):
+        """Pinned host buffers (W: m x k, H: n x k), adjacent in one allocation."""
+        whh = torch.zeros((self.obs.m + self.obs.n) * self.k, dtype=self.dt).pin_memory()
+        return (whh[: self.obs.m * self.k].view(self.obs.m, self.k),
+                whh[self.obs.m * self.k:].view(self.obs.n, self.k))
+
+    def run_host(self, w_host: torch.Tensor, h_host: torch.Tensor, *, graph: bool = True):
+        """H2D of the host factors into resident device factors, the sweep, and
+        one D2H of the packed results [sums | RH | RtW]; returns pinned host
+        views (sums, RH, RtW), valid once the current stream reaches this
+        point. With ``graph`` the sequence is captured once per (host buffers,
+        stream) as a CUDA graph and replayed."""
+        for t, rows in ((w_host, self.obs.m), (h_host, self.obs.n)):
+            if t.device.type != "cpu" or t.dtype != self.dt or tuple(t.shape) != (rows, self.k) \
+                    or not t.is_contiguous():
+                raise ValueError(f"host factor must be a contiguous CPU ({rows} x {self.k}) {self.dt} tensor")
+        m, n, k, ld = self.obs.m, self.obs.n, self.k, self.ld
+        if getattr(self, "_host", None) is None:
+            dev = self.obs.dev.device
+            self._whd = torch.zeros((m + n) * ld, dtype=self.dt, device=dev)
+            self._wd = self._whd[: m * ld].view(m, ld)
+            self._hd = self._whd[m * ld:].view(n, ld)
+            self._host = torch.empty(self._out.numel(), dtype=torch.uint8).pin_memory()
+            nb_rh = self.RH.numel() * 4
+            self._host_views = (self._host[:24].view(torch.float64),
+                                self._host[32:32 + nb_rh].view(self.dt).view(m, k),
+                                self._host[32 + nb_rh:].view(self.dt).view(n, k))
+            self._graph_key = None
+        stream = torch.cuda.current_stream()
+        if not graph or getattr(self, "_no_graph", False):
+            self._host_call(w_host, h_host)
+            return self._host_views
+        key = (w_host.data_ptr(), h_host.data_ptr(), stream.cuda_stream)
+        if self._graph_key != key:
+            self._host_call(w_host, h_host)          # warm-up, eager
+            torch.cuda.synchronize()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+                    self._host_call(w_host, h_host)
+            except RuntimeError:
+                torch.cuda.synchronize()
+                self._no_graph = True
+                return self._host_views
+            stream.wait_stream(side)
+            self._graph, self._graph_key = g, key
+        self._graph.replay()
+        return self._host_views
+
+    def _host_call(self, w_host, h_host):
+        m, n, k, ld = self.obs.m, self.obs.n, self.k, self.ld
+        adjacent = (ld == k and h_host.data_ptr() == w_host.data_ptr() + m * k * 4
+                    and w_host.untyped_storage().data_ptr() == h_host.untyped_storage().data_ptr())
+        if adjacent:
+            flat = torch.as_strided(w_host, ((m + n) * k,), (1,))
+            self._whd.copy_(flat, non_blocking=True)
+        else:
+            self._wd[:, :k].copy_(w_host, non_blocking=True)
+            self._hd[:, :k].copy_(h_host, non_blocking=True)
+        self.run(self._wd, self._hd)
+        self._host.copy_(self._out, non_blocking=True)
+
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
         lib = _lib.lib()
         st = _lib.stream_ptr()
@@ -345,3 +412,46 @@ class HybridSweepPlan:
         if self.want_r:
             _lib.check(lib.mfg_gather(_lib.MFG_F32, self.obs.size, self._rsrc.data_ptr(),
                                       self._rcat.data_ptr(), self.R.data_ptr(), st), "R gather")
+
+
+def best_sweep_plan(obs: ObservationSet, k: int, *, want_r: bool = True, out_scale: float = 1.0,
+                    mode: str | None = None):
+    """The faster of the gather-only sweep (``mfsolver.SweepPlan``) and the
+    hybrid panel sweep for this Omega and k, decided by timing both once
+    (3 sweeps each on seeded factors). ``mode`` / ``MFG_SWEEP_PLAN``:
+    "gather", "hybrid" or "auto" (default). The hybrid plan is considered for
+    fp32 storage, a supported width and at least ``MFG_HYBRID_MIN_NNZ``
+    (2e7) entries."""
+    from .mfsolver import SweepPlan
+
+    mode = mode or os.environ.get("MFG_SWEEP_PLAN", "auto")
+    base = SweepPlan(obs, k, want_r=want_r, out_scale=out_scale)
+    base.kind = "gather"
+    eligible = (obs.dtype == torch.float32 and panel_ld(k, obs.dtype) > 0
+                and (mode == "hybrid" or obs.size >= int(float(os.environ.get("MFG_HYBRID_MIN_NNZ", 2e7)))))
+    if mode == "gather" or not eligible:
+        return base
+    hyb = HybridSweepPlan(obs, k, want_r=want_r, out_scale=out_scale)
+    if mode == "hybrid":
+        return hyb
+    g = torch.Generator(device="cpu").manual_seed(1234)
+    dev = obs.dev.device
+    w = base.pad((torch.rand((obs.m, k), generator=g) * 0.5).to(dev))
+    h = base.pad((torch.rand((obs.n, k), generator=g) * 0.5).to(dev))
+
+    def t(plan):
+        best = float("inf")
+        for i in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            plan.run(w, h)
+            e1.record()
+            e1.synchronize()
+            if i >= 2:
+                best = min(best, e0.elapsed_time(e1))
+        return best
+
+    tb, th = t(base), t(hyb)
+    pick = hyb if th < tb else base
+    pick.trial_ms = {"gather": tb, "hybrid": th}
+    return pick

@@ -92,3 +92,37 @@ def test_hybrid_rejects_unsupported():
     obs32 = obs64.with_dtype(torch.float32)
     with pytest.raises(ValueError):
         HybridSweepPlan(obs32, 20)
+
+
+def test_hybrid_run_host_and_plan_choice():
+    """End to end from pinned host factors (eager and as a replayed CUDA graph)
+    equals the resident run; best_sweep_plan returns a plan of either kind
+    with the same results."""
+    from paper_2204_14067_b200.panel import HybridSweepPlan, best_sweep_plan
+    k = 40
+    m, n, r, c, v = synth.generate("c3", scale=0.03, seed=77)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    obs = D.ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
+    w, h = synth.sweep_factors(m, n, k, seed=5)
+    plan = HybridSweepPlan(obs, k)
+    wt = torch.as_tensor(w).float().cuda()
+    ht = torch.as_tensor(h).float().cuda()
+    plan.run(plan.pad(wt), plan.pad(ht))
+    ref = [plan.sums.clone().cpu(), plan.RH.clone().cpu(), plan.RtW.clone().cpu()]
+    wa, ha = plan.pinned_factors()
+    wa.copy_(torch.as_tensor(w).float())
+    ha.copy_(torch.as_tensor(h).float())
+    wh = torch.as_tensor(w).float().pin_memory()
+    hh = torch.as_tensor(h).float().pin_memory()
+    for (a, b) in ((wa, ha), (wh, hh)):
+        for graph in (False, True, True):
+            out = plan.run_host(a, b, graph=graph)
+            torch.cuda.synchronize()
+            for x, y in zip(out, ref):
+                assert torch.equal(x, y)
+    for mode in ("gather", "hybrid", "auto"):
+        p = best_sweep_plan(obs, k, mode=mode)
+        assert p.kind == (mode if mode != "auto" else p.kind)
+        p.run(p.pad(wt), p.pad(ht))
+        assert torch.allclose(p.RH.cpu(), ref[1], rtol=0, atol=2e-4 * float(ref[1].abs().max()))
+        assert float(p.sums[0]) == pytest.approx(float(ref[0][0]), rel=1e-6)
