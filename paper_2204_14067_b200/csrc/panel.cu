@@ -37,6 +37,8 @@
 // writes its partial output vector to its slot; k_panel_fold adds a self row's
 // slots in slot order to the cold part, so the result does not depend on which
 // CTA ran which piece (bitwise reproducible).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "engine.cuh"
 
@@ -324,6 +326,207 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(const PanelArgs A) {
   }
 }
 
+// ---- 4-lane groups (rows of one 32-dim block, k <= 40) --------------------
+// The same walk with a row on 4 lanes (8 groups, i.e. 8 pieces, per warp and
+// 32 entries per warp batch): a lane holds two 16-byte chunks of each of the 4
+// rows of a batch, so the reduce-scatter / all-gather of the 4 dots costs 7
+// shuffles per 32 entries instead of 8 per 16 -- shuffles share the shared-
+// memory data pipe that bounds this kernel -- and the batch costs ~110
+// instructions per 32 entries. Even groups read chunks [0,4) then [4,8) of
+// their rows, odd groups the opposite halves, so the two rows of a quarter
+// warp never share banks.
+constexpr int kPT4 = 512;                 // 16 warps, <= 128 registers
+constexpr int kRing4Bytes = (kPT4 / 32) * 8 * 2 * kBlockBytes;
+constexpr int kPanel4Bytes = 202 * 1024;
+constexpr int kPanel4Smem = kPanel4Bytes + kRing4Bytes;
+
+template <int KT>
+__global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int KC = 8 + KT;
+  constexpr int KP = KC * 4;
+  float* s_main = reinterpret_cast<float*>(smem_raw);
+  float* s_tail = s_main + (size_t)A.PR * 32;
+  __shared__ int s_left;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, g = lane >> 2;
+  const int cA = q + 4 * (g & 1), cB = q + 4 * ((g & 1) ^ 1);   // this lane's two main chunks
+  const int e_mine = (q >> 1) + 2 * (q & 1);                    // the entry this lane finishes
+  unsigned char* ring = smem_raw + kPanel4Bytes + (warp * 8 + g) * 2 * kBlockBytes;
+  const unsigned a_mA = (unsigned)__cvta_generic_to_shared(s_main) + cA * 16;
+  const unsigned a_mB = (unsigned)__cvta_generic_to_shared(s_main) + cB * 16;
+  const unsigned a_tail = (unsigned)__cvta_generic_to_shared(s_tail) + (q & 1) * 16;
+  const unsigned a_ring = (unsigned)__cvta_generic_to_shared(ring);
+  const bool hi1 = (q & 2) != 0, odd = (q & 1) != 0;
+  const int gb = lane & 28;
+  int li = A.cta_start[blockIdx.x];
+  for (int step = 0; step < A.n_list; ++step, li = li + 1 == A.n_list ? 0 : li + 1) {
+    const int4 it = A.plist[li];        // {pass, panel, first piece, end piece}
+    const int npc = it.w - it.z;
+    __syncthreads();                    // everyone is done with the previous panel
+    if (tid == 0) s_left = npc - *reinterpret_cast<volatile int*>(A.counters + li);
+    __syncthreads();
+    if (s_left <= 0) continue;          // this panel's pieces are all taken
+    const PanelPass& P = A.p[it.x];
+    {
+      const int32_t* ids = P.panel_ids + (size_t)it.y * A.PR;
+      const int total = A.PR * KC;
+      for (int c = tid; c < total; c += kPT4) {
+        const int r = c / KC, ch = c - r * KC;
+        const int gid = ids[r];
+        float* dst = ch < 8 ? s_main + (size_t)r * 32 + ch * 4
+                            : s_tail + (size_t)r * KT * 4 + (ch - 8) * 4;
+        if (gid >= 0) cp16(dst, P.gath + (size_t)gid * P.ldg + ch * 4);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_commit();
+      cp_wait<0>();
+    }
+    __syncthreads();
+    float* const rhot = P.rhot;
+    const bool want_sq = P.psq != nullptr;
+    auto take = [&]() {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(A.counters + li, 8);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto load_desc = [&](int t0) {
+      int4 d = make_int4(0, 0, 0, -1);  // {self row, first block, length, slot}; slot < 0: none
+      if (t0 + g < npc) d = P.pieces[it.z + t0 + g];
+      return d;
+    };
+    auto load_self = [&](const int4& d, float4& xa, float4& xb, float4& xt) {
+      const float* srow = P.self + (size_t)d.x * P.lds;
+      xa = *reinterpret_cast<const float4*>(srow + cA * 4);
+      xb = *reinterpret_cast<const float4*>(srow + cB * 4);
+      if (KT > 0) xt = *reinterpret_cast<const float4*>(srow + 32 + (q & 1) * 4);
+    };
+    int t_cur = take();
+    int4 pc = load_desc(t_cur);
+    float4 hA, hB, ht = make_float4(0.f, 0.f, 0.f, 0.f);
+    load_self(pc, hA, hB, ht);
+    while (t_cur < npc) {
+      const int t_nxt = take();
+      const int4 pcn = load_desc(t_nxt);
+      float4 hAn, hBn, htn = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int len = pc.z;
+      const int lim = len - e_mine;     // batch b holds this lane's entry iff 4 b < lim
+      float* rh = rhot + (size_t)pc.y * 16 + e_mine;
+      float4 aA = make_float4(0.f, 0.f, 0.f, 0.f), aB = aA, at = aA;
+      double sq = 0.0;
+      const int nb = (len + 3) >> 2;
+      const int nblk = (nb + 3) >> 2;
+      int nbw = nb;
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 4));
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 8));
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 16));
+      const int nblkw = (nbw + 3) >> 2;
+      const int4* rp = P.recs + (size_t)pc.y * 6;
+      const int jmax = max(nblk - 1, 0);
+      // the group's 4 lanes copy a 96-byte block as 6 chunks: lanes 0, 1 take two
+      auto fetch = [&](int slot, int jb) {
+        cp16(ring + slot * kBlockBytes + q * 16, rp + jb * 6 + q);
+        if (q < 2) cp16(ring + slot * kBlockBytes + (q + 4) * 16, rp + jb * 6 + q + 4);
+      };
+      fetch(0, 0);
+      cp_commit();
+      for (int j = 0; j < nblkw; ++j) {
+        fetch((j + 1) & 1, min(j + 1, jmax));   // clamped: short pieces re-read their last block
+        cp_commit();
+        cp_wait<1>();
+        __syncwarp();
+        if (j == 0) load_self(pcn, hAn, hBn, htn);
+        const unsigned rs = a_ring + (j & 1) * kBlockBytes;
+#pragma unroll 1
+        for (int bb = 0; bb < 4; ++bb) {
+          const int b = j * 4 + bb;
+          if (b >= nbw) break;
+          const uint2 lw = lds64(rs + bb * 8);
+          const float a_mine = lds32(rs + 32 + (bb * 4 + e_mine) * 4);
+          const unsigned l0 = lw.x & 0xffffu, l1 = lw.x >> 16, l2 = lw.y & 0xffffu, l3 = lw.y >> 16;
+          const float4 mA0 = lds128(a_mA + l0 * 128), mB0 = lds128(a_mB + l0 * 128);
+          const float4 mA1 = lds128(a_mA + l1 * 128), mB1 = lds128(a_mB + l1 * 128);
+          const float4 mA2 = lds128(a_mA + l2 * 128), mB2 = lds128(a_mB + l2 * 128);
+          const float4 mA3 = lds128(a_mA + l3 * 128), mB3 = lds128(a_mB + l3 * 128);
+          float4 tA = make_float4(0.f, 0.f, 0.f, 0.f), tB = tA;
+          if (KT > 0) {
+            // tail chunk q&1 of entries q>>1 and (q>>1) + 2
+            tA = lds128(a_tail + (hi1 ? l1 : l0) * (KT * 16));
+            tB = lds128(a_tail + (hi1 ? l3 : l2) * (KT * 16));
+          }
+          const float p0 = dot4(mA0, hA) + dot4(mB0, hB);
+          const float p1 = dot4(mA1, hA) + dot4(mB1, hB);
+          const float p2 = dot4(mA2, hA) + dot4(mB2, hB);
+          const float p3 = dot4(mA3, hA) + dot4(mB3, hB);
+          // reduce-scatter over the 4 lanes: lanes with q&2 keep entries {1,3},
+          // the others {0,2}; then q&1 picks the upper one (fixed tree)
+          float klo = hi1 ? p1 : p0, khi = hi1 ? p3 : p2;
+          const float slo = hi1 ? p0 : p1, shi = hi1 ? p2 : p3;
+          klo += __shfl_xor_sync(0xffffffffu, slo, 2);
+          khi += __shfl_xor_sync(0xffffffffu, shi, 2);
+          if (KT > 0) {
+            klo += dot4(tA, ht);
+            khi += dot4(tB, ht);
+          }
+          float kk = odd ? khi : klo;
+          const float ss = odd ? klo : khi;
+          kk += __shfl_xor_sync(0xffffffffu, ss, 1);
+          const bool valid = b * 4 < lim;
+          const float r = valid ? kk - a_mine : 0.f;
+          // entry e lives in lane (e & 1) * 2 + (e >> 1) of the group
+          const float r0 = __shfl_sync(0xffffffffu, r, gb);
+          const float r1 = __shfl_sync(0xffffffffu, r, gb + 2);
+          const float r2 = __shfl_sync(0xffffffffu, r, gb + 1);
+          const float r3 = __shfl_sync(0xffffffffu, r, gb + 3);
+          axpy4(aA, r0, mA0); axpy4(aB, r0, mB0);
+          axpy4(aA, r1, mA1); axpy4(aB, r1, mB1);
+          axpy4(aA, r2, mA2); axpy4(aB, r2, mB2);
+          axpy4(aA, r3, mA3); axpy4(aB, r3, mB3);
+          if (KT > 0) {
+            axpy4(at, hi1 ? r1 : r0, tA);
+            axpy4(at, hi1 ? r3 : r2, tB);
+          }
+          if (rhot != nullptr && valid) rh[b * 4] = r;
+          if (want_sq) sq = fma((double)r, (double)r, sq);
+        }
+        __syncwarp();
+      }
+      cp_wait<0>();
+      if (nblkw == 0) load_self(pcn, hAn, hBn, htn);
+      if (KT > 0) {   // lanes q and q ^ 2 hold the same tail chunk
+        at.x += __shfl_xor_sync(0xffffffffu, at.x, 2);
+        at.y += __shfl_xor_sync(0xffffffffu, at.y, 2);
+        at.z += __shfl_xor_sync(0xffffffffu, at.z, 2);
+        at.w += __shfl_xor_sync(0xffffffffu, at.w, 2);
+      }
+      if (want_sq) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+      }
+      if (pc.w >= 0) {
+        float* o = P.po + (size_t)pc.w * KP;
+        *reinterpret_cast<float4*>(o + cA * 4) = aA;
+        *reinterpret_cast<float4*>(o + cB * 4) = aB;
+        if (KT > 0 && q < KT) *reinterpret_cast<float4*>(o + 32 + q * 4) = at;
+        if (want_sq && q == 0) P.psq[pc.w] = sq;
+      }
+      __syncwarp();
+      pc = pcn;
+      t_cur = t_nxt;
+      hA = hAn; hB = hBn; ht = htn;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int d = atomicAdd(A.counters + A.n_list, 1);
+    if (d == (int)gridDim.x - 1) {
+      for (int i = 0; i <= A.n_list; ++i) A.counters[i] = 0;
+    }
+  }
+}
+
 // out[row] += scale * sum of the row's piece outputs, in slot order.
 // Threads are (sub-range, row, 16-byte chunk): a block takes 256 / (KC * S)
 // self rows, each row's slots cut into S contiguous sub-ranges whose partial
@@ -437,6 +640,19 @@ int launch_panel(const PanelArgs& A, cudaStream_t stream) {
   return MFG_OK;
 }
 
+template <int KT>
+int launch_panel4(const PanelArgs& A, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    MFG_CUDA_CHECK(cudaFuncSetAttribute(k_panel4<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kPanel4Smem));
+    configured = true;
+  }
+  k_panel4<KT><<<kNumSMs, kPT4, kPanel4Smem, stream>>>(A);
+  MFG_LAUNCH_CHECK();
+  return MFG_OK;
+}
+
 bool panel_shape(int ld, int* nb, int* kt) {
   if (ld == 40) { *nb = 1; *kt = 2; return true; }
   if (ld == 32) { *nb = 1; *kt = 0; return true; }
@@ -452,7 +668,8 @@ using namespace mfg;
 extern "C" int mfg_panel_rows(int ld) {
   int nb, kt;
   if (!panel_shape(ld, &nb, &kt)) return 0;
-  return (kPanelBytes / ((nb * 8 + kt) * 16)) & ~1;
+  // rows of one 32-dim block run on 4-lane groups (k_panel4), k = 64 on 8-lane groups
+  return ((nb == 1 ? kPanel4Bytes : kPanelBytes) / ((nb * 8 + kt) * 16)) & ~1;
 }
 
 extern "C" int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const int32_t* cta_start,
@@ -483,8 +700,12 @@ extern "C" int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const i
   A.PR = mfg_panel_rows(ld);
   A.counters = counters;
   cudaStream_t s = (cudaStream_t)stream;
-  if (nb == 1 && kt == 2) return launch_panel<1, 2>(A, s);
-  if (nb == 1 && kt == 0) return launch_panel<1, 0>(A, s);
+  if (getenv("MFG_PANEL_GL8")) {   // A/B: the 8-lane-group kernel for every width
+    if (nb == 1 && kt == 2) return launch_panel<1, 2>(A, s);
+    if (nb == 1 && kt == 0) return launch_panel<1, 0>(A, s);
+  }
+  if (nb == 1 && kt == 2) return launch_panel4<2>(A, s);
+  if (nb == 1 && kt == 0) return launch_panel4<0>(A, s);
   return launch_panel<2, 0>(A, s);
 }
 
