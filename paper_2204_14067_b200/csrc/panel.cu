@@ -336,8 +336,10 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(const PanelArgs A) {
 // their rows, odd groups the opposite halves, so the two rows of a quarter
 // warp never share banks.
 constexpr int kPT4 = 512;                 // 16 warps, <= 128 registers
-constexpr int kRing4Bytes = (kPT4 / 32) * 8 * 2 * kBlockBytes;
-constexpr int kPanel4Bytes = 202 * 1024;
+constexpr int kRing4Stride = 2 * kBlockBytes + 16;   // per group; 52 words: the 8 groups' slots fall in distinct banks
+constexpr int kRing4Bytes = (kPT4 / 32) * 8 * kRing4Stride;
+constexpr int kPanel4Bytes = 200 * 1024;
+static_assert(kPanel4Bytes + kRing4Bytes + 64 <= 232448, "k_panel4 shared memory");
 constexpr int kPanel4Smem = kPanel4Bytes + kRing4Bytes;
 
 template <int KT>
@@ -353,12 +355,13 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
   const int q = lane & 3, g = lane >> 2;
   const int cA = q + 4 * (g & 1), cB = q + 4 * ((g & 1) ^ 1);   // this lane's two main chunks
   const int e_mine = (q >> 1) + 2 * (q & 1);                    // the entry this lane finishes
-  unsigned char* ring = smem_raw + kPanel4Bytes + (warp * 8 + g) * 2 * kBlockBytes;
+  unsigned char* ring = smem_raw + kPanel4Bytes + (warp * 8 + g) * kRing4Stride;
   const unsigned a_mA = (unsigned)__cvta_generic_to_shared(s_main) + cA * 16;
   const unsigned a_mB = (unsigned)__cvta_generic_to_shared(s_main) + cB * 16;
   const unsigned a_tail = (unsigned)__cvta_generic_to_shared(s_tail) + (q & 1) * 16;
   const unsigned a_ring = (unsigned)__cvta_generic_to_shared(ring);
   const bool hi1 = (q & 2) != 0, odd = (q & 1) != 0;
+  const bool gpar = (g & 1) != 0;       // odd groups load their tails in the opposite order
   const int gb = lane & 28;
   int li = A.cta_start[blockIdx.x];
   for (int step = 0; step < A.n_list; ++step, li = li + 1 == A.n_list ? 0 : li + 1) {
@@ -449,11 +452,15 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
           const float4 mA1 = lds128(a_mA + l1 * 128), mB1 = lds128(a_mB + l1 * 128);
           const float4 mA2 = lds128(a_mA + l2 * 128), mB2 = lds128(a_mB + l2 * 128);
           const float4 mA3 = lds128(a_mA + l3 * 128), mB3 = lds128(a_mB + l3 * 128);
+          // tail chunk q&1 of entries q>>1 (lo) and (q>>1) + 2 (hi). The layout
+          // build orders a batch's entries by bank window (local row mod 4), so an
+          // even group reading its lo pair while the odd group of the same quarter
+          // warp reads its hi pair touches 4 different windows.
           float4 tA = make_float4(0.f, 0.f, 0.f, 0.f), tB = tA;
           if (KT > 0) {
-            // tail chunk q&1 of entries q>>1 and (q>>1) + 2
-            tA = lds128(a_tail + (hi1 ? l1 : l0) * (KT * 16));
-            tB = lds128(a_tail + (hi1 ? l3 : l2) * (KT * 16));
+            const unsigned llo = hi1 ? l1 : l0, lhi = hi1 ? l3 : l2;
+            tA = lds128(a_tail + (gpar ? lhi : llo) * (KT * 16));
+            tB = lds128(a_tail + (gpar ? llo : lhi) * (KT * 16));
           }
           const float p0 = dot4(mA0, hA) + dot4(mB0, hB);
           const float p1 = dot4(mA1, hA) + dot4(mB1, hB);
@@ -466,8 +473,9 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
           klo += __shfl_xor_sync(0xffffffffu, slo, 2);
           khi += __shfl_xor_sync(0xffffffffu, shi, 2);
           if (KT > 0) {
-            klo += dot4(tA, ht);
-            khi += dot4(tB, ht);
+            const float dA = dot4(tA, ht), dB = dot4(tB, ht);
+            klo += gpar ? dB : dA;
+            khi += gpar ? dA : dB;
           }
           float kk = odd ? khi : klo;
           const float ss = odd ? klo : khi;
@@ -484,8 +492,9 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
           axpy4(aA, r2, mA2); axpy4(aB, r2, mB2);
           axpy4(aA, r3, mA3); axpy4(aB, r3, mB3);
           if (KT > 0) {
-            axpy4(at, hi1 ? r1 : r0, tA);
-            axpy4(at, hi1 ? r3 : r2, tB);
+            const float rlo = hi1 ? r1 : r0, rhi = hi1 ? r3 : r2;
+            axpy4(at, gpar ? rhi : rlo, tA);
+            axpy4(at, gpar ? rlo : rhi, tB);
           }
           if (rhot != nullptr && valid) rh[b * 4] = r;
           if (want_sq) sq = fma((double)r, (double)r, sq);

@@ -3,7 +3,7 @@ export PYTHONDONTWRITEBYTECODE=1
 export MFG_SYNTH_CACHE=/tmp/synth
 tag=${TAG:-r2p}
 MFG_PROBE_QUICK=1 python tools/panel_probe.py ${WL:-c4} > gpurun_out/${tag}_plain.log 2>&1 || { tail gpurun_out/${tag}_plain.log; exit 1; }
-MFG_PROBE_QUICK=1 ncu --set full --clock-control none --import-source on -k k_panel -s 0 -c 1 -f \
+MFG_PROBE_QUICK=1 ncu --set full --clock-control none --import-source on -k regex:"^k_panel4?$" -s 0 -c 1 -f \
     -o gpurun_out/${tag}_k_panel python tools/panel_probe.py ${WL:-c4} > gpurun_out/${tag}_ncu.log 2>&1
 echo "k_panel rc=$?"
 if [ -n "$FOLD" ]; then
