@@ -243,7 +243,7 @@ class HybridSweepPlan:
         if not self.ld:
             raise ValueError(f"HybridSweepPlan: unsupported factor width k={k}")
         env = os.environ.get
-        lmin = int(env("MFG_PANEL_LMIN", 8)) if lmin is None else lmin
+        lmin = int(env("MFG_PANEL_LMIN", 16)) if lmin is None else lmin
         lmax = int(env("MFG_PANEL_LMAX", 256)) if lmax is None else lmax
         max_panels = int(env("MFG_PANEL_MAXP", 64)) if max_panels is None else max_panels
         if min_panel_entries is None:

@@ -1,0 +1,91 @@
+"""Host logic of the hybrid sweep's panel layout (paper_2204_14067_b200/panel.py):
+the arrays the panel kernel walks, replayed in numpy, reproduce the reference's
+R and R.H (mfg/data.py:253-263, mfg/operators.py:108) on the hot entries, and
+hot + cold entries partition Omega. Runs on CPU tensors (no GPU)."""
+import types
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2204_14067_b200 import panel
+
+
+def _case(seed, m, n, dens, decay):
+    rng = np.random.default_rng(seed)
+    mask = rng.random((m, n)) < (dens * (1.0 / (1 + np.arange(n))) ** decay)[None, :]
+    rows, cols = np.nonzero(mask)
+    vals = rng.standard_normal(len(rows)).astype(np.float32)
+    return rng, rows, cols, vals
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(PR=16, lmin=3, lmax=21, max_panels=6, min_panel_entries=10),
+    dict(PR=8, lmin=1, lmax=5, max_panels=100, min_panel_entries=1),
+    dict(PR=64, lmin=2, lmax=500, max_panels=2, min_panel_entries=1),
+])
+def test_panel_layout_replay(cfg):
+    m, n, k = 60, 300, 40
+    rng, rows, cols, vals = _case(0, m, n, 0.5, 0.4)
+    nnz = len(rows)
+    lay = types.SimpleNamespace(nnz=nnz, nrows=m, ncols=n, idx=torch.tensor(cols, dtype=torch.int32),
+                                row_of=torch.tensor(rows, dtype=torch.int32))
+    PR = cfg.pop("PR")
+    pp = panel._PanelPass(lay, torch.tensor(vals), m, n, PR, k, 0, want_r=False, want_sq=True, **cfg)
+    assert pp.n_hot > 0
+    W = rng.standard_normal((m, k))
+    H = rng.standard_normal((n, k))
+    ids = pp.panel_ids.numpy()
+    pieces = pp.pieces.numpy()
+    recs = pp.recs.numpy()
+    loc16 = recs.view(np.int16).reshape(-1, 48)
+    po = np.zeros((pp.n_pieces, k))
+    rhot = np.zeros((pp.n_blocks + 2) * 16)
+    seen = np.zeros(pp.n_pieces, int)
+    covered = np.zeros(pp.n_pieces, int)
+    for _, p, a, b in pp.plist.numpy():
+        prow = ids[p * PR:(p + 1) * PR]
+        covered[a:b] += 1
+        assert np.all(np.diff(pieces[a:b, 2]) <= 0)          # longest first inside a panel
+        for t in range(a, b):
+            row, blk0, ln, slot = pieces[t]
+            assert 1 <= ln <= cfg["lmax"]
+            seen[slot] += 1
+            for e in range(ln):
+                blk, off = blk0 + e // 16, e % 16
+                g = prow[loc16[blk, off]]
+                assert g >= 0
+                a_e = float(recs[blk, 8 + off:9 + off].view(np.float32)[0])
+                r = float(W[row] @ H[g]) - a_e
+                rhot[blk * 16 + off] = r
+                po[slot] += r * H[g]
+    assert np.all(seen == 1) and np.all(covered == 1)
+    assert int(pp.plist_entries.sum()) == pp.n_hot
+    # fold in slot order + the cold entries = R.H of the whole Omega
+    RH = np.zeros((m, k))
+    fr, fb, fc = pp.frows.numpy(), pp.fbeg.numpy(), pp.fcnt.numpy()
+    assert len(set(fr.tolist())) == len(fr)
+    assert np.all(fc[:pp.n_light] <= 32) and np.all(fc[pp.n_light:] > 32)
+    for f, row in enumerate(fr):
+        RH[row] += po[fb[f]:fb[f] + fc[f]].sum(0)
+    cold = pp.cold_mask.numpy()
+    Rfull = (W[rows] * H[cols]).sum(1) - vals.astype(np.float64)
+    np.add.at(RH, rows[cold], Rfull[cold, None] * H[cols[cold]])
+    RHref = np.zeros((m, k))
+    np.add.at(RHref, rows, Rfull[:, None] * H[cols])
+    assert np.abs(RH - RHref).max() < 1e-11
+    # the residual map back to CSR order
+    ho, hp = pp.hot_orig.numpy(), pp.hot_pos.numpy()
+    assert len(ho) + int(cold.sum()) == nnz and not cold[ho].any()
+    assert np.abs(rhot[hp] - Rfull[ho]).max() < 1e-12
+
+
+def test_panel_layout_no_hot_entries():
+    m, n, k = 10, 40, 40
+    rng, rows, cols, vals = _case(3, m, n, 0.3, 0.0)
+    lay = types.SimpleNamespace(nnz=len(rows), nrows=m, ncols=n, idx=torch.tensor(cols, dtype=torch.int32),
+                                row_of=torch.tensor(rows, dtype=torch.int32))
+    pp = panel._PanelPass(lay, torch.tensor(vals), m, n, 16, k, 1, lmin=10 ** 6, lmax=256, max_panels=4,
+                          min_panel_entries=1, want_r=False, want_sq=False)
+    assert pp.n_hot == 0 and pp.n_pieces == 0 and pp.plist.shape[0] == 0
+    assert bool(pp.cold_mask.all())
