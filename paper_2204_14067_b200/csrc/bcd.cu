@@ -753,7 +753,7 @@ int build_split(const mfg_layout* lay, Carver& c, const RowSched& rs, int grid, 
 
 
 // ---------------------------------------------------------------------------
-// Warp-per-row BCD with the Gram on the fp64 tensor cores (round 2, k <= 40).
+// Warp-per-row BCD with the Gram on the fp64 tensor cores (round 2, k <= 64).
 //
 // One warp owns one row (or one segment of a heavy row) at a time and takes
 // it from a warp-granular ticket (longest first, as above), so a short row
@@ -781,8 +781,11 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-constexpr int kDmWarps = 4;            // warps per CTA
-constexpr int kDmMaxK = 40;            // k handled by the DMMA kernel (5 tiles)
+constexpr int kDmMaxK = 64;            // k handled by the DMMA kernel (8 tiles)
+// warps per CTA: 4 up to k = 40; 3 for k = 41..64, where a warp's slab is up
+// to 37.9 KB (two CTAs = 6 warps fill an SM's shared memory) and the 2 NP
+// accumulators take up to 144 registers
+__host__ __device__ constexpr int dm_warps(int nt) { return nt <= 5 ? 4 : 3; }
 #ifndef MFG_BCD_DM_MINB
 #define MFG_BCD_DM_MINB 4              // CTAs per SM (128 registers)
 #endif
@@ -805,10 +808,12 @@ size_t dm_smem_per_warp(int k) {
 // CTAs per SM of an instantiation (NT = 5: 3 CTAs with 168 registers was
 // slower than 4 with 128 at c4, CSR 11.7 -> 12.4 ms, CSC 19.4 -> 22.0 ms)
 template <int NT>
-__host__ __device__ constexpr int dm_minb() { return NT >= 5 ? MFG_BCD_DM_MINB5 : MFG_BCD_DM_MINB; }
+__host__ __device__ constexpr int dm_minb() {
+  return NT >= 6 ? 2 : (NT >= 5 ? MFG_BCD_DM_MINB5 : MFG_BCD_DM_MINB);
+}
 
 template <typename TS, int NT>
-__global__ void __launch_bounds__(32 * kDmWarps, dm_minb<NT>())
+__global__ void __launch_bounds__(32 * dm_warps(NT), dm_minb<NT>())
 k_bcd_dm(mfg_layout lay, int k, const TS* __restrict__ vals, const TS* __restrict__ other, int ldo,
          double lam, TS* __restrict__ out, int ldout, int* __restrict__ bad,
          const int* __restrict__ order, int* __restrict__ ticket, SplitPlan sp) {
@@ -1128,16 +1133,17 @@ template <typename TS>
 int launch_dm(const mfg_layout* lay, int k, const TS* vals, const TS* other, int ldo, double lam,
               TS* out, int ldout, int* bad, const RowSched& rs, const SplitPlan& sp,
               cudaStream_t stream) {
-  const size_t smem = dm_smem_per_warp(k) * kDmWarps;
   const int nt = (k + 7) / 8;
-  int grid = (lay->nrows + kDmWarps - 1) / kDmWarps;
-  const int full = kNumSMs * (nt >= 5 ? MFG_BCD_DM_MINB5 : MFG_BCD_DM_MINB);
+  const int wpc = dm_warps(nt);
+  const size_t smem = dm_smem_per_warp(k) * wpc;
+  int grid = (lay->nrows + wpc - 1) / wpc;
+  const int full = kNumSMs * (nt >= 6 ? 2 : (nt >= 5 ? MFG_BCD_DM_MINB5 : MFG_BCD_DM_MINB));
   if (grid > full) grid = full;
   if (grid < 1) grid = 1;
   auto go = [&](auto kern) -> int {
     if (smem > 48 * 1024)
       MFG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 32 * kDmWarps, smem, stream>>>(*lay, k, vals, other, ldo, lam, out, ldout, bad,
+    kern<<<grid, 32 * wpc, smem, stream>>>(*lay, k, vals, other, ldo, lam, out, ldout, bad,
                                                 rs.order, rs.ticket, sp);
     MFG_LAUNCH_CHECK();
     return MFG_OK;
@@ -1148,9 +1154,12 @@ int launch_dm(const mfg_layout* lay, int k, const TS* vals, const TS* other, int
     case 3: return go(k_bcd_dm<TS, 3>);
     case 4: return go(k_bcd_dm<TS, 4>);
     case 5: return go(k_bcd_dm<TS, 5>);
+    case 6: return go(k_bcd_dm<TS, 6>);
+    case 7: return go(k_bcd_dm<TS, 7>);
+    case 8: return go(k_bcd_dm<TS, 8>);
     default: break;
   }
-  set_error("bcd: DMMA path supports k <= 40");
+  set_error("bcd: DMMA path supports k <= 64");
   return MFG_ERR_ARG;
 }
 

@@ -107,7 +107,7 @@ def _bcd_instance(seed, m=300, n=2000, heavy=(2000, 1500, 700, 300)):
     return rng, m, n, r, c, v
 
 
-@pytest.mark.parametrize("k", [1, 5, 20, 24, 25, 30, 40, 41, 64])
+@pytest.mark.parametrize("k", [1, 5, 20, 24, 25, 30, 40, 41, 48, 56, 64, 65])
 def test_bcd_fp32_storage_matches_oracle(k):
     """The fp32-storage instantiation (k_bcd<float,...>, what every c2-c5 MF
     phase runs): fp32 A and factors, fp64 Gram + Cholesky, fp32 rows out.

@@ -290,7 +290,7 @@ def test_bcd_large_k_packed_and_dual(k):
     assert np.max(np.abs(_np(out.h) - h1)) < 1e-9 * max(1.0, np.abs(h1).max())
 
 
-@pytest.mark.parametrize("k", [1, 4, 5, 20, 37, 40, 41, 64, 128])
+@pytest.mark.parametrize("k", [1, 4, 5, 20, 37, 40, 41, 49, 57, 64, 65, 128])
 def test_bcd_split_heavy_rows(k):
     """Rows with more than S = max(256, nnz/grid) entries are cut into
     segments whose partial Grams are summed in segment order by the CTA that
