@@ -210,11 +210,26 @@ int mfg_panel_ctas(void);
 int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const int32_t* cta_start,
                     const mfg_panel_pass* csr, const mfg_panel_pass* csc, const void* W,
                     const void* H, int32_t* counters, void* stream);
-/* out[row] += out_scale * (sum of the row's piece outputs, slot order);
+/* out[row] += out_scale * (sum of the row's piece outputs, slot order), for
+ * the rows that own slots; assign != 0: out[row] = ... instead (every entry of
+ * those rows is in a piece: the cold pieces of mfg_cold_sweep share the slots).
  * sums[0] += sum of piece_sq (when both are non-NULL; sq_ws: 1 KB of zeroed
  * device scratch, left zeroed).                                            */
 int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* out, int ldout,
-                   double out_scale, double* sums, void* sq_ws, void* stream);
+                   double out_scale, int assign, double* sums, void* sq_ws, void* stream);
+
+/* The cold entries of both passes walked like panel pieces, their rows read
+ * with global loads (ld = 32 or 40). The structs' pieces / recs / r_hot
+ * describe the cold pieces (record blocks: 16 x u32 gathered-row ids, then
+ * 16 x f32 A, 128 B; 2 blocks of padding); piece_out / piece_sq are the
+ * arrays of the panel passes (slots are shared); panel_ids, frows, fbeg and
+ * fcnt are not read. A piece whose length field has bit 30 set is its self
+ * row's only slot: out_scale times its vector goes straight to that row of
+ * RH / RtW (row stride ld; only used when k == ld) and the row is not in the
+ * fold lists. counters: 3 zeroed int32 (left zeroed).                      */
+int mfg_cold_sweep(int ld, const mfg_panel_pass* csr, const mfg_panel_pass* csc,
+                   const void* W, const void* H, void* RH, void* RtW, double out_scale,
+                   int32_t* counters, void* stream);
 
 /* ---- SDDMM with fused reductions --------------------------------------
  * p_e = sum_d L[row_e, d] * (scale ? scale[d] : 1) * Rt[col_e, d]

@@ -97,7 +97,8 @@ _SIGS = {
     "mfg_panel_rows": (_INT, [_INT]),
     "mfg_panel_ctas": (_INT, []),
     "mfg_panel_sweep": (_INT, [_INT, _INT, _P, _P, _PP, _PP, _P, _P, _P, _P]),
-    "mfg_panel_fold": (_INT, [_INT, _INT, _PP, _P, _INT, _D, _P, _P, _P]),
+    "mfg_cold_sweep": (_INT, [_INT, _PP, _PP, _P, _P, _P, _P, _D, _P, _P]),
+    "mfg_panel_fold": (_INT, [_INT, _INT, _PP, _P, _INT, _D, _INT, _P, _P, _P]),
     "mfg_sddmm_workspace": (_SZ, [_LP, _INT]),
     "mfg_sddmm": (_INT, [_INT, _INT, _LP, _INT, _P, _INT, _P, _P, _INT, _P, _P, _D, _P, _P, _P,
                          _SZ, _P]),

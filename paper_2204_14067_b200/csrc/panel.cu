@@ -536,7 +536,205 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
   }
 }
 
-// out[row] += scale * sum of the row's piece outputs, in slot order.
+// ---- cold entries: the same piece walk on global loads --------------------
+// Entries whose gathered row is not panelled, or whose piece is too short, are
+// cut into pieces per self row as well (a self row's cold entries in their
+// original order, at most Lmax each) and walked by 4-lane groups with the
+// batch loop of k_panel4 -- the rows come through L2 / L1 (`ld.global.nc`)
+// instead of shared memory, 10 LDG.128 per lane and batch in flight. Record
+// blocks hold global row ids: 16 x u32, then 16 x f32 (128 B). Warps take
+// rounds of 8 pieces from one ticket per pass; there is no CTA-wide step.
+constexpr int kCT = 512;
+constexpr int kColdBlock = 128;
+constexpr int kColdRingStride = 2 * kColdBlock + 16;   // 68 words: 8 groups on distinct banks
+constexpr int kColdSmem = (kCT / 32) * 8 * kColdRingStride;
+
+struct ColdArgs {
+  PanelPass p[2];
+  float* out[2];            // RH / RtW: rows whose only slot is a cold piece are written here
+  float scale;
+  int npieces[2];
+  int* counters;            // [2] piece tickets, [1] finished CTAs (zero at rest)
+};
+
+__device__ __forceinline__ float4 ldg128(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kCT, 1) k_cold4(const ColdArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int KP = (8 + KT) * 4;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int q = lane & 3, g = lane >> 2;
+  const int cA = q, cB = q + 4;         // this lane's two main chunks
+  const int e_mine = (q >> 1) + 2 * (q & 1);
+  unsigned char* ring = smem_raw + (warp * 8 + g) * kColdRingStride;
+  const unsigned a_ring = (unsigned)__cvta_generic_to_shared(ring);
+  const bool hi1 = (q & 2) != 0, odd = (q & 1) != 0;
+  const int gb = lane & 28;
+  for (int pass = 0; pass < 2; ++pass) {
+    const PanelPass& P = A.p[pass];
+    const int npc = A.npieces[pass];
+    if (npc <= 0) continue;
+    float* const rhot = P.rhot;
+    const bool want_sq = P.psq != nullptr;
+    const float* const gath = P.gath;
+    const int ldg = P.ldg;
+    auto take = [&]() {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(A.counters + pass, 8);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto load_desc = [&](int t0) {
+      int4 d = make_int4(0, 0, 0, -1);  // {self row, first block, length, slot}; slot < 0: none
+      if (t0 + g < npc) d = P.pieces[t0 + g];
+      return d;
+    };
+    auto load_self = [&](const int4& d, float4& xa, float4& xb, float4& xt) {
+      const float* srow = P.self + (size_t)d.x * P.lds;
+      xa = *reinterpret_cast<const float4*>(srow + cA * 4);
+      xb = *reinterpret_cast<const float4*>(srow + cB * 4);
+      if (KT > 0) xt = *reinterpret_cast<const float4*>(srow + 32 + (q & 1) * 4);
+    };
+    int t_cur = take();
+    int4 pc = load_desc(t_cur);
+    float4 hA, hB, ht = make_float4(0.f, 0.f, 0.f, 0.f);
+    load_self(pc, hA, hB, ht);
+    while (t_cur < npc) {
+      const int t_nxt = take();
+      const int4 pcn = load_desc(t_nxt);
+      float4 hAn, hBn, htn = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int len = pc.z & 0x3fffffff;
+      const bool direct = (pc.z >> 30) != 0;   // the row's only slot: write the output row itself
+      const int lim = len - e_mine;
+      float* rh = rhot + (size_t)pc.y * 16 + e_mine;
+      float4 aA = make_float4(0.f, 0.f, 0.f, 0.f), aB = aA, at = aA;
+      double sq = 0.0;
+      const int nb = (len + 3) >> 2;
+      const int nblk = (nb + 3) >> 2;
+      int nbw = nb;
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 4));
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 8));
+      nbw = max(nbw, __shfl_xor_sync(0xffffffffu, nbw, 16));
+      const int nblkw = (nbw + 3) >> 2;
+      const int4* rp = P.recs + (size_t)pc.y * 8;
+      const int jmax = max(nblk - 1, 0);
+      auto fetch = [&](int slot, int jb) {   // 8 chunks of a 128-byte block on 4 lanes
+        cp16(ring + slot * kColdBlock + q * 16, rp + jb * 8 + q);
+        cp16(ring + slot * kColdBlock + (q + 4) * 16, rp + jb * 8 + q + 4);
+      };
+      fetch(0, 0);
+      cp_commit();
+      for (int j = 0; j < nblkw; ++j) {
+        fetch((j + 1) & 1, min(j + 1, jmax));
+        cp_commit();
+        cp_wait<1>();
+        __syncwarp();
+        if (j == 0) load_self(pcn, hAn, hBn, htn);
+        const unsigned rs = a_ring + (j & 1) * kColdBlock;
+#pragma unroll 1
+        for (int bb = 0; bb < 4; ++bb) {
+          const int b = j * 4 + bb;
+          if (b >= nbw) break;
+          uint4 iw;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(iw.x), "=r"(iw.y), "=r"(iw.z), "=r"(iw.w) : "r"(rs + bb * 16));
+          const float a_mine = lds32(rs + 64 + (bb * 4 + e_mine) * 4);
+          const float* g0 = gath + (size_t)iw.x * ldg;
+          const float* g1 = gath + (size_t)iw.y * ldg;
+          const float* g2 = gath + (size_t)iw.z * ldg;
+          const float* g3 = gath + (size_t)iw.w * ldg;
+          const float4 mA0 = ldg128(g0 + cA * 4), mB0 = ldg128(g0 + cB * 4);
+          const float4 mA1 = ldg128(g1 + cA * 4), mB1 = ldg128(g1 + cB * 4);
+          const float4 mA2 = ldg128(g2 + cA * 4), mB2 = ldg128(g2 + cB * 4);
+          const float4 mA3 = ldg128(g3 + cA * 4), mB3 = ldg128(g3 + cB * 4);
+          float4 tA = make_float4(0.f, 0.f, 0.f, 0.f), tB = tA;
+          if (KT > 0) {
+            tA = ldg128((hi1 ? g1 : g0) + 32 + (q & 1) * 4);
+            tB = ldg128((hi1 ? g3 : g2) + 32 + (q & 1) * 4);
+          }
+          const float p0 = dot4(mA0, hA) + dot4(mB0, hB);
+          const float p1 = dot4(mA1, hA) + dot4(mB1, hB);
+          const float p2 = dot4(mA2, hA) + dot4(mB2, hB);
+          const float p3 = dot4(mA3, hA) + dot4(mB3, hB);
+          float klo = hi1 ? p1 : p0, khi = hi1 ? p3 : p2;
+          const float slo = hi1 ? p0 : p1, shi = hi1 ? p2 : p3;
+          klo += __shfl_xor_sync(0xffffffffu, slo, 2);
+          khi += __shfl_xor_sync(0xffffffffu, shi, 2);
+          if (KT > 0) {
+            klo += dot4(tA, ht);
+            khi += dot4(tB, ht);
+          }
+          float kk = odd ? khi : klo;
+          const float ss = odd ? klo : khi;
+          kk += __shfl_xor_sync(0xffffffffu, ss, 1);
+          const bool valid = b * 4 < lim;
+          const float r = valid ? kk - a_mine : 0.f;
+          const float r0 = __shfl_sync(0xffffffffu, r, gb);
+          const float r1 = __shfl_sync(0xffffffffu, r, gb + 2);
+          const float r2 = __shfl_sync(0xffffffffu, r, gb + 1);
+          const float r3 = __shfl_sync(0xffffffffu, r, gb + 3);
+          axpy4(aA, r0, mA0); axpy4(aB, r0, mB0);
+          axpy4(aA, r1, mA1); axpy4(aB, r1, mB1);
+          axpy4(aA, r2, mA2); axpy4(aB, r2, mB2);
+          axpy4(aA, r3, mA3); axpy4(aB, r3, mB3);
+          if (KT > 0) {
+            axpy4(at, hi1 ? r1 : r0, tA);
+            axpy4(at, hi1 ? r3 : r2, tB);
+          }
+          if (rhot != nullptr && valid) rh[b * 4] = r;
+          if (want_sq) sq = fma((double)r, (double)r, sq);
+        }
+        __syncwarp();
+      }
+      cp_wait<0>();
+      if (nblkw == 0) load_self(pcn, hAn, hBn, htn);
+      if (KT > 0) {
+        at.x += __shfl_xor_sync(0xffffffffu, at.x, 2);
+        at.y += __shfl_xor_sync(0xffffffffu, at.y, 2);
+        at.z += __shfl_xor_sync(0xffffffffu, at.z, 2);
+        at.w += __shfl_xor_sync(0xffffffffu, at.w, 2);
+      }
+      if (want_sq) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+      }
+      if (pc.w >= 0) {
+        float* o = P.po + (size_t)pc.w * KP;
+        if (direct) {
+          o = A.out[pass] + (size_t)pc.x * KP;
+          const float sc = A.scale;
+          aA.x *= sc; aA.y *= sc; aA.z *= sc; aA.w *= sc;
+          aB.x *= sc; aB.y *= sc; aB.z *= sc; aB.w *= sc;
+          at.x *= sc; at.y *= sc; at.z *= sc; at.w *= sc;
+        }
+        *reinterpret_cast<float4*>(o + cA * 4) = aA;
+        *reinterpret_cast<float4*>(o + cB * 4) = aB;
+        if (KT > 0 && q < KT) *reinterpret_cast<float4*>(o + 32 + q * 4) = at;
+        if (want_sq && q == 0) P.psq[pc.w] = sq;
+      }
+      __syncwarp();
+      pc = pcn;
+      t_cur = t_nxt;
+      hA = hAn; hB = hBn; ht = htn;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int d = atomicAdd(A.counters + 2, 1);
+    if (d == (int)gridDim.x - 1) {
+      A.counters[0] = 0;
+      A.counters[1] = 0;
+      A.counters[2] = 0;
+    }
+  }
+}
+
+// out[row] += scale * sum of the row's piece outputs, in slot order (assign:
+// out[row] = ..., when every entry of the row is in a piece).
 // Threads are (sub-range, row, 16-byte chunk): a block takes 256 / (KC * S)
 // self rows, each row's slots cut into S contiguous sub-ranges whose partial
 // sums are added in sub-range order (a fixed tree). Light rows (few slots)
@@ -546,7 +744,7 @@ __global__ void __launch_bounds__(256)
 k_panel_fold(int n_rows, int n_row_blocks, int S, const int32_t* __restrict__ frows,
              const int32_t* __restrict__ fbeg, const int32_t* __restrict__ fcnt,
              const float* __restrict__ po, int KC, int k, float* __restrict__ out, int ldout,
-             float scale) {
+             float scale, int assign) {
   __shared__ float4 s_part[256];
   {
     const int rpb = 256 / (KC * S);
@@ -597,7 +795,7 @@ k_panel_fold(int n_rows, int n_row_blocks, int S, const int32_t* __restrict__ fr
       float* o = out + (size_t)frows[f] * ldout + ch * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (ch * 4 + e < k) o[e] = o[e] + scale * tot[e];
+        if (ch * 4 + e < k) o[e] = assign ? scale * tot[e] : o[e] + scale * tot[e];
     }
   }
 }
@@ -721,7 +919,8 @@ extern "C" int mfg_panel_sweep(int ld, int n_list, const int32_t* plist, const i
 extern "C" int mfg_panel_ctas(void) { return kNumSMs; }
 
 extern "C" int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* out, int ldout,
-                              double out_scale, double* sums, void* sq_ws, void* stream) {
+                              double out_scale, int assign, double* sums, void* sq_ws,
+                              void* stream) {
   int nb, kt;
   MFG_REQUIRE(panel_shape(ld, &nb, &kt), "panel fold: unsupported factor row width");
   MFG_REQUIRE(pass && out, "panel fold: null argument");
@@ -735,14 +934,14 @@ extern "C" int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* o
     const int nrb = (nl + rpb - 1) / rpb;
     k_panel_fold<<<nrb, 256, 0, st>>>(nl, nrb, 1, pass->frows, pass->fbeg, pass->fcnt,
                                       (const float*)pass->piece_out, KC, k, (float*)out, ldout,
-                                      (float)out_scale);
+                                      (float)out_scale, assign);
     MFG_LAUNCH_CHECK();
   }
   if (nh > 0) {
     const int S = 256 / KC;   // one row per block
     k_panel_fold<<<nh, 256, 0, st>>>(nh, nh, S, pass->frows + nl, pass->fbeg + nl,
                                      pass->fcnt + nl, (const float*)pass->piece_out, KC, k,
-                                     (float*)out, ldout, (float)out_scale);
+                                     (float*)out, ldout, (float)out_scale, assign);
     MFG_LAUNCH_CHECK();
   }
   if (pass->piece_sq != nullptr && sums != nullptr) {
@@ -752,5 +951,43 @@ extern "C" int mfg_panel_fold(int ld, int k, const mfg_panel_pass* pass, void* o
                                           (unsigned int*)(bp + kSqBlocks), sums);
     MFG_LAUNCH_CHECK();
   }
+  return MFG_OK;
+}
+
+/* The cold pieces of both passes on global loads (k_cold4). The passes'
+ * structs carry the cold piece table, the cold record blocks (16 x u32 row
+ * ids, 16 x f32 values), the residual buffer in record order, and the same
+ * piece_out / piece_sq arrays as the panel passes (slots are shared).      */
+extern "C" int mfg_cold_sweep(int ld, const mfg_panel_pass* csr, const mfg_panel_pass* csc,
+                              const void* W, const void* H, void* RH, void* RtW, double out_scale,
+                              int32_t* counters, void* stream) {
+  int nb, kt;
+  MFG_REQUIRE(panel_shape(ld, &nb, &kt) && nb == 1, "cold sweep: unsupported factor row width");
+  MFG_REQUIRE(csr && csc && counters, "cold sweep: null argument");
+  if (csr->n_pieces <= 0 && csc->n_pieces <= 0) return MFG_OK;
+  ColdArgs A;
+  const mfg_panel_pass* pp[2] = {csr, csc};
+  for (int i = 0; i < 2; ++i) {
+    PanelPass& P = A.p[i];
+    P.self = (const float*)(i == 0 ? W : H);
+    P.gath = (const float*)(i == 0 ? H : W);
+    P.panel_ids = nullptr;
+    P.pieces = (const int4*)pp[i]->pieces;
+    P.recs = (const int4*)pp[i]->recs;
+    P.rhot = (float*)pp[i]->r_hot;
+    P.po = (float*)pp[i]->piece_out;
+    P.psq = (double*)pp[i]->piece_sq;
+    P.lds = ld;
+    P.ldg = ld;
+    A.npieces[i] = pp[i]->n_pieces;
+  }
+  A.out[0] = (float*)RH;
+  A.out[1] = (float*)RtW;
+  A.scale = (float)out_scale;
+  A.counters = counters;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (kt == 2) k_cold4<2><<<kNumSMs, kCT, kColdSmem, s>>>(A);
+  else k_cold4<0><<<kNumSMs, kCT, kColdSmem, s>>>(A);
+  MFG_LAUNCH_CHECK();
   return MFG_OK;
 }

@@ -42,12 +42,33 @@ def panel_ld(k: int, dtype) -> int:
     return ld if ld and _lib.lib().mfg_panel_rows(ld) > 0 else 0
 
 
+def _cut(lens, prow, ppan, lmax, dev):
+    """Cut pieces into sub-pieces of at most lmax entries (balanced lengths).
+    Returns (srow, span, slen, cstart): self row, panel, length and first
+    compact entry of every sub-piece, in piece order."""
+    npieces = int(lens.numel())
+    nsub = (lens + lmax - 1) // lmax
+    pid = torch.repeat_interleave(torch.arange(npieces, device=dev), nsub)
+    ns = int(pid.numel())
+    first_sub = torch.cumsum(nsub, 0) - nsub
+    j = torch.arange(ns, device=dev) - first_sub[pid]
+    base = lens[pid] // nsub[pid]
+    rem = lens[pid] % nsub[pid]
+    slen = base + (j < rem).long()
+    cstart_piece = torch.cumsum(lens, 0) - lens          # compact start of each piece
+    cstart = cstart_piece[pid] + j * base + torch.minimum(j, rem)
+    return prow[pid], ppan[pid], slen, cstart
+
+
 class _PanelPass:
-    """One pass's hot layout (device arrays) + its ctypes ``mfg_panel_pass``."""
+    """One pass's layout (device arrays): the hot pieces of the panels with
+    their ctypes ``mfg_panel_pass`` (``c``), and -- with ``cold_pieces`` --
+    the cold entries cut into pieces for ``mfg_cold_sweep`` (``cc``)."""
 
     def __init__(self, lay: _LayoutBuffers, vals: torch.Tensor, n_self: int, n_gath: int, PR: int,
                  ld: int, pass_id: int, *, lmin: int, lmax: int,
-                 max_panels: int, min_panel_entries: int, want_r: bool, want_sq: bool):
+                 max_panels: int, min_panel_entries: int, want_r: bool, want_sq: bool,
+                 cold_pieces: bool = False, direct: bool = False):
         dev = vals.device
         nnz = lay.nnz
         idx = lay.idx[:nnz].long()
@@ -97,23 +118,10 @@ class _PanelPass:
         cold[hot_orig] = False
         self.cold_mask = cold
         # kept pieces -> sub-pieces of at most lmax entries
-        lens = plen[keep_piece]
-        prow = rows_s[pstart][keep_piece]
-        ppan = ppanel[keep_piece]
+        srow, span, slen, cstart = _cut(plen[keep_piece], rows_s[pstart][keep_piece],
+                                        ppanel[keep_piece], lmax, dev)
         del rows_s, pstart, plen, ppanel, keep_piece
-        npieces = int(lens.numel())
-        nsub = (lens + lmax - 1) // lmax
-        pid = torch.repeat_interleave(torch.arange(npieces, device=dev), nsub)
-        ns = int(pid.numel())
-        first_sub = torch.cumsum(nsub, 0) - nsub
-        j = torch.arange(ns, device=dev) - first_sub[pid]
-        base = lens[pid] // nsub[pid]
-        rem = lens[pid] % nsub[pid]
-        slen = base + (j < rem).long()
-        cstart_piece = torch.cumsum(lens, 0) - lens          # compact start of each piece
-        cstart = cstart_piece[pid] + j * base + torch.minimum(j, rem)
-        srow = prow[pid]
-        span = ppan[pid]
+        ns = int(srow.numel())
         nblk = (slen + 15) // 16                             # record blocks of each sub-piece
         bstart = torch.cumsum(nblk, 0) - nblk                # first block of each sub-piece
         n_blocks = int(nblk.sum().item()) if ns else 0
@@ -158,25 +166,77 @@ class _PanelPass:
         nrows_hot = min(npk * PR, n_gath)
         ids[:nrows_hot] = order[:nrows_hot].to(torch.int32)
         self.panel_ids = ids
-        del rank, order, idx, row_of, local
-        # slots in (self row, panel, run) order
-        seq = torch.arange(ns, device=dev)
-        o_rs = torch.argsort(srow * max(ns, 1) + seq)
-        slot = torch.empty(ns, dtype=torch.long, device=dev)
+        del rank, order, local
+        # cold pieces: a self row's cold entries in their order, cut at lmax;
+        # record blocks of 16 x u32 gathered-row ids + 16 x f32 values
+        nsc = 0
+        if cold_pieces:
+            cold_orig = torch.nonzero(cold).flatten()
+            ncold = int(cold_orig.numel())
+            crow = row_of[cold_orig]
+            fc = torch.ones(ncold, dtype=torch.bool, device=dev)
+            if ncold > 1:
+                fc[1:] = crow[1:] != crow[:-1]
+            cps = torch.nonzero(fc).flatten()
+            cpl = torch.diff(cps, append=torch.tensor([ncold], device=dev))
+            srow_c, span_c, slen_c, cstart_c = _cut(cpl, crow[cps], torch.full_like(cps, npk), lmax, dev)
+            nsc = int(srow_c.numel())
+            nblk_c = (slen_c + 15) // 16
+            bstart_c = torch.cumsum(nblk_c, 0) - nblk_c
+            nbc = int(nblk_c.sum().item()) if nsc else 0
+            sub_c = torch.repeat_interleave(torch.arange(nsc, device=dev), slen_c)
+            cpos = bstart_c[sub_c] * 16 + (torch.arange(ncold, device=dev) - cstart_c[sub_c])
+            del sub_c, fc, crow
+            crecs = torch.zeros((nbc + 2, 32), dtype=torch.int32, device=dev)
+            if ncold:
+                blk, off = cpos // 16, cpos % 16
+                crecs[blk, off] = idx[cold_orig].to(torch.int32)
+                crecs[blk, 16 + off] = vals[:nnz][cold_orig].contiguous().view(torch.int32)
+                del blk, off
+            self.cold_recs, self.cold_orig, self.cold_pos, self.n_cold_blocks = crecs, cold_orig, cpos, nbc
+            srow_all = torch.cat([srow, srow_c])
+        else:
+            srow_all = srow
+        del idx, row_of
+        # slots in (self row, panel, run) order; the cold pieces of a row come last
+        nsa = ns + nsc
+        seq = torch.arange(nsa, device=dev)
+        o_rs = torch.argsort(srow_all * max(nsa, 1) + seq)
+        slot = torch.empty(nsa, dtype=torch.long, device=dev)
         slot[o_rs] = seq
-        frows, counts = torch.unique_consecutive(srow[o_rs], return_counts=True)
+        frows, counts = torch.unique_consecutive(srow_all[o_rs], return_counts=True)
         fbeg = torch.cumsum(counts, 0) - counts
+        direct_c = None
+        if cold_pieces and direct and nsc:
+            # a self row whose only slot is a cold piece: the piece writes the
+            # output row itself (bit 30 of its length) and the row needs no fold
+            rowcount = torch.zeros(n_self, dtype=torch.long, device=dev)
+            rowcount.index_add_(0, srow_all, torch.ones_like(srow_all))
+            direct_c = rowcount[srow_c] == 1
+            row_direct = torch.zeros(n_self, dtype=torch.bool, device=dev)
+            row_direct[srow_c[direct_c]] = True
+            keep_f = ~row_direct[frows]
+            frows, counts, fbeg = frows[keep_f], counts[keep_f], fbeg[keep_f]
+            del rowcount, row_direct, keep_f
         # light rows (<= 32 slots) first, heavy rows after them
         o_lh = torch.argsort((counts > 32).to(torch.int8), stable=True)
-        self.n_light = int((counts <= 32).sum().item()) if ns else 0
+        self.n_light = int((counts <= 32).sum().item()) if counts.numel() else 0
         self.frows = frows[o_lh].to(torch.int32)
         self.fbeg = fbeg[o_lh].to(torch.int32)
         self.fcnt = counts[o_lh].to(torch.int32)
         # piece table: per panel by decreasing length
         o_pl = torch.argsort(span * (lmax + 1) + (lmax - slen), stable=True)
-        pieces = torch.stack([srow[o_pl], bstart[o_pl], slen[o_pl], slot[o_pl]], dim=1).to(torch.int32)
+        pieces = torch.stack([srow[o_pl], bstart[o_pl], slen[o_pl], slot[:ns][o_pl]], dim=1).to(torch.int32)
         self.pieces = pieces.contiguous() if ns else torch.zeros((1, 4), dtype=torch.int32, device=dev)
         self.n_pieces = ns
+        self.n_slots = nsa
+        if cold_pieces:
+            o_c = torch.argsort(lmax - slen_c, stable=True)
+            lenf = slen_c if direct_c is None else slen_c + direct_c.long() * (1 << 30)
+            self.n_direct = 0 if direct_c is None else int(direct_c.sum().item())
+            cp = torch.stack([srow_c[o_c], bstart_c[o_c], lenf[o_c], slot[ns:][o_c]], dim=1).to(torch.int32)
+            self.cold_pieces = cp.contiguous() if nsc else torch.zeros((1, 4), dtype=torch.int32, device=dev)
+            self.n_cold_pieces = nsc
         # panel list: {pass, panel, first piece, end piece} + entries per element
         span_s = span[o_pl]
         if ns:
@@ -191,19 +251,27 @@ class _PanelPass:
         else:
             self.plist = torch.zeros((0, 4), dtype=torch.int32, device=dev)
             self.plist_entries = torch.zeros(0, dtype=torch.long)
-        # outputs / scratch
+        # outputs / scratch (slots are shared by the hot and the cold pieces)
         self.r_hot = torch.zeros((n_blocks + 2) * 16, dtype=torch.float32, device=dev) if want_r else None
-        self.piece_out = torch.empty((max(ns, 1), ld), dtype=torch.float32, device=dev)
-        self.piece_sq = torch.zeros(max(ns, 1), dtype=torch.float64, device=dev) if want_sq else None
-        self.c = _lib.PanelPass(ns, int(self.frows.numel()), self.n_light, self.panel_ids.data_ptr(),
+        self.piece_out = torch.empty((max(nsa, 1), ld), dtype=torch.float32, device=dev)
+        self.piece_sq = torch.zeros(max(nsa, 1), dtype=torch.float64, device=dev) if want_sq else None
+        self.c = _lib.PanelPass(nsa, int(self.frows.numel()), self.n_light, self.panel_ids.data_ptr(),
                                 self.pieces.data_ptr(), self.recs.data_ptr(),
                                 self.frows.data_ptr(), self.fbeg.data_ptr(), self.fcnt.data_ptr(),
                                 _lib.ptr(self.r_hot),
                                 self.piece_out.data_ptr(), _lib.ptr(self.piece_sq))
+        if cold_pieces:
+            self.cc = _lib.PanelPass(nsc, 0, 0, None, self.cold_pieces.data_ptr(),
+                                     self.cold_recs.data_ptr(), None, None, None, None,
+                                     self.piece_out.data_ptr(), _lib.ptr(self.piece_sq))
 
     @property
     def ref(self):
         return ctypes.byref(self.c)
+
+    @property
+    def cold_ref(self):
+        return ctypes.byref(self.cc)
 
 
 def _cold_layout(lay: _LayoutBuffers, vals: torch.Tensor, cold: torch.Tensor):
@@ -234,7 +302,8 @@ class HybridSweepPlan:
 
     def __init__(self, obs: ObservationSet, k: int, *, want_r: bool = True, out_scale: float = 1.0,
                  lmin: int | None = None, lmax: int | None = None,
-                 max_panels: int | None = None, min_panel_entries: int | None = None):
+                 max_panels: int | None = None, min_panel_entries: int | None = None,
+                 cold: str | None = None):
         if obs.dtype != torch.float32:
             raise ValueError("HybridSweepPlan: fp32 storage only")
         self.obs, self.k = obs, int(k)
@@ -245,7 +314,7 @@ class HybridSweepPlan:
         env = os.environ.get
         lmin = int(env("MFG_PANEL_LMIN", 16)) if lmin is None else lmin
         lmax = int(env("MFG_PANEL_LMAX", 256)) if lmax is None else lmax
-        max_panels = int(env("MFG_PANEL_MAXP", 64)) if max_panels is None else max_panels
+        max_panels = int(env("MFG_PANEL_MAXP", 32)) if max_panels is None else max_panels
         if min_panel_entries is None:
             min_panel_entries = int(env("MFG_PANEL_MINE", min(100_000, max(1, obs.size // 256))))
         lib = _lib.lib()
@@ -254,7 +323,18 @@ class HybridSweepPlan:
         self.out_scale = float(out_scale)
         if lmax > 511:
             raise ValueError("HybridSweepPlan: lmax must be <= 511")
-        kw = dict(lmin=lmin, lmax=lmax, max_panels=max_panels, min_panel_entries=min_panel_entries)
+        # cold entries: "pieces" walks them like panel pieces on global loads
+        # (k_cold4; rows of one 32-dim block), "gather" runs the grouped gather
+        # kernel on their sub-layouts
+        cold = cold or env("MFG_PANEL_COLD", "pieces")
+        if cold not in ("pieces", "gather"):
+            raise ValueError("cold must be 'pieces' or 'gather'")
+        if self.ld == 64:
+            cold = "gather"
+        self.cold = cold
+        lean = cold == "pieces"
+        kw = dict(lmin=lmin, lmax=lmax, max_panels=max_panels, min_panel_entries=min_panel_entries,
+                  cold_pieces=lean, direct=lean and self.ld == self.k)
         self.p0 = _PanelPass(dev.csr, dev.vals, obs.m, obs.n, self.PR, self.ld, 0, want_r=False,
                              want_sq=True, **kw)
         self.p1 = _PanelPass(dev.csc, dev.vals_csc, obs.n, obs.m, self.PR, self.ld, 1,
@@ -273,26 +353,36 @@ class HybridSweepPlan:
             self.plist = torch.zeros((1, 4), dtype=torch.int32, device=dev.device)
             start = torch.zeros(nctas, dtype=torch.long)
         self.cta_start = start.to(torch.int32).to(dev.device)
-        self.cold_csr, self.cold_vals = _cold_layout(dev.csr, dev.vals, self.p0.cold_mask)
-        self.cold_csc, self.cold_vals_csc = _cold_layout(dev.csc, dev.vals_csc, self.p1.cold_mask)
         nnz = obs.size
         self.want_r = want_r
+        nh_pad = (self.p0.n_blocks + 2) * 16
+        if lean:
+            ncold_r = (self.p0.n_cold_blocks + 2) * 16
+        else:
+            self.cold_csr, self.cold_vals = _cold_layout(dev.csr, dev.vals, self.p0.cold_mask)
+            self.cold_csc, self.cold_vals_csc = _cold_layout(dev.csc, dev.vals_csc, self.p1.cold_mask)
+            ncold_r = self.cold_csr.nnz + OMEGA_PAD
         if want_r:
-            # R in CSR order = gather from [hot residuals (padded order) | cold residuals]
-            nh_pad = (self.p0.n_blocks + 2) * 16
-            self._rcat = torch.zeros(nh_pad + self.cold_csr.nnz + OMEGA_PAD, dtype=self.dt,
-                                     device=dev.device)
+            # R in CSR order = gather from [hot residuals | cold residuals], both in record order
+            self._rcat = torch.zeros(nh_pad + ncold_r, dtype=self.dt, device=dev.device)
             self.p0.r_hot = self._rcat[:nh_pad]
             self.p0.c.r_hot = self.p0.r_hot.data_ptr()
             self._rcold = self._rcat[nh_pad:]
             src = torch.empty(nnz, dtype=torch.int32, device=dev.device)
             src[self.p0.hot_orig] = self.p0.hot_pos.to(torch.int32)
-            cold_pos = torch.nonzero(self.p0.cold_mask).flatten()
-            src[cold_pos] = (nh_pad + torch.arange(cold_pos.numel(), device=dev.device)).to(torch.int32)
+            if lean:
+                self.p0.cc.r_hot = self._rcold.data_ptr()
+                src[self.p0.cold_orig] = (nh_pad + self.p0.cold_pos).to(torch.int32)
+            else:
+                cold_pos = torch.nonzero(self.p0.cold_mask).flatten()
+                src[cold_pos] = (nh_pad + torch.arange(cold_pos.numel(), device=dev.device)).to(torch.int32)
             self._rsrc = src
             self.R = torch.empty(nnz, dtype=self.dt, device=dev.device)
         else:
             self.R = None
+        if lean:
+            for p in (self.p0, self.p1):
+                del p.cold_orig, p.cold_pos
         for p in (self.p0, self.p1):
             del p.hot_orig, p.hot_pos, p.cold_mask
         es = 4
@@ -302,14 +392,22 @@ class HybridSweepPlan:
         self.sums = self._out[:24].view(torch.float64)
         self.RH = self._out[32:32 + nb_rh].view(self.dt).view(obs.m, self.k)
         self.RtW = self._out[32 + nb_rh:].view(self.dt).view(obs.n, self.k)
-        self.wsb = lib.mfg_sweep_workspace(self.cold_csr.ref, self.cold_csc.ref, self.k)
+        if lean:
+            self.wsb = 1 << 16        # the two norms (mfg_dot)
+            self.cold_counters = torch.zeros(4, dtype=torch.int32, device=dev.device)
+        else:
+            self.wsb = lib.mfg_sweep_workspace(self.cold_csr.ref, self.cold_csc.ref, self.k)
         self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
         self.counters = torch.zeros(self.n_list + 2, dtype=torch.int32, device=dev.device)
         self.sq_ws = torch.zeros(1024, dtype=torch.uint8, device=dev.device)
+        self._side = torch.cuda.Stream(device=dev.device)
+        self._ev_fork = torch.cuda.Event()
+        self._ev_join = torch.cuda.Event()
         self.stats = {
             "panel_rows": self.PR, "csr_panels": self.p0.n_panels, "csc_panels": self.p1.n_panels,
             "csr_hot": self.p0.n_hot, "csc_hot": self.p1.n_hot, "nnz": nnz,
             "csr_pieces": self.p0.n_pieces, "csc_pieces": self.p1.n_pieces, "lmax": lmax,
+            "cold": ("pieces on global loads (k_cold4)" if lean else "gather kernel (k_sweep_g8f)"),
         }
 
     def pad(self, f: torch.Tensor) -> torch.Tensor:
@@ -391,27 +489,54 @@ class HybridSweepPlan:
         st = _lib.stream_ptr()
         if int(w.stride(0)) != self.ld or int(h.stride(0)) != self.ld:
             raise ValueError(f"factors must have row stride {self.ld}")
-        # cold entries: grouped gather kernel; also the dense norms and the row zeroing
-        _lib.check(lib.mfg_sweep_sharded(
-            _lib.MFG_F32, 0, self.cold_csr.ref, self.cold_csc.ref, self.k,
-            self.cold_vals.data_ptr(), self.cold_vals_csc.data_ptr(),
-            w.data_ptr(), w.data_ptr(), self.ld, h.data_ptr(), h.data_ptr(), self.ld,
-            self._rcold.data_ptr() if self.want_r else None, self.RH.data_ptr(),
-            self.RtW.data_ptr(), self.out_scale, self.sums.data_ptr(), self.ws.data_ptr(),
-            self.wsb, st), "hybrid sweep (cold)")
+        lean = self.cold == "pieces"
+        if lean:
+            # Every row with entries is the fold of its slots (assigned, not added);
+            # rows without entries are never written and stay zero. The norms.
+            self.sums[0:1].zero_()
+            for x, o in ((w, 1), (h, 2)):
+                _lib.check(lib.mfg_dot(_lib.MFG_F32, x.shape[0] * self.ld, x.data_ptr(), x.data_ptr(),
+                                       self.sums.data_ptr() + 8 * o, self.ws.data_ptr(), self.wsb, st),
+                           "norm")
+            _lib.check(lib.mfg_cold_sweep(self.ld, self.p0.cold_ref, self.p1.cold_ref, w.data_ptr(),
+                                          h.data_ptr(), self.RH.data_ptr(), self.RtW.data_ptr(),
+                                          self.out_scale, self.cold_counters.data_ptr(), st),
+                       "cold sweep")
+        else:
+            # cold entries: grouped gather kernel; also the dense norms and the row zeroing
+            _lib.check(lib.mfg_sweep_sharded(
+                _lib.MFG_F32, 0, self.cold_csr.ref, self.cold_csc.ref, self.k,
+                self.cold_vals.data_ptr(), self.cold_vals_csc.data_ptr(),
+                w.data_ptr(), w.data_ptr(), self.ld, h.data_ptr(), h.data_ptr(), self.ld,
+                self._rcold.data_ptr() if self.want_r else None, self.RH.data_ptr(),
+                self.RtW.data_ptr(), self.out_scale, self.sums.data_ptr(), self.ws.data_ptr(),
+                self.wsb, st), "hybrid sweep (cold)")
         if self.n_list:
             _lib.check(lib.mfg_panel_sweep(self.ld, self.n_list, self.plist.data_ptr(),
                                            self.cta_start.data_ptr(), self.p0.ref, self.p1.ref,
                                            w.data_ptr(), h.data_ptr(), self.counters.data_ptr(), st),
                        "panel sweep")
-            _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p0.ref, self.RH.data_ptr(), self.k,
-                                          self.out_scale, self.sums.data_ptr(), self.sq_ws.data_ptr(), st),
-                       "panel fold")
-            _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p1.ref, self.RtW.data_ptr(), self.k,
-                                          self.out_scale, None, None, st), "panel fold")
+        # R back to CSR order on a side stream, next to the folds (both are short,
+        # latency- and DRAM-bound kernels; in a captured graph: parallel branches)
+        side = None
         if self.want_r:
+            cur = torch.cuda.current_stream()
+            side = self._side
+            self._ev_fork.record(cur)
+            side.wait_event(self._ev_fork)
             _lib.check(lib.mfg_gather(_lib.MFG_F32, self.obs.size, self._rsrc.data_ptr(),
-                                      self._rcat.data_ptr(), self.R.data_ptr(), st), "R gather")
+                                      self._rcat.data_ptr(), self.R.data_ptr(), side.cuda_stream),
+                       "R gather")
+            self._ev_join.record(side)
+        if self.n_list or lean:
+            _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p0.ref, self.RH.data_ptr(), self.k,
+                                          self.out_scale, 1 if lean else 0, self.sums.data_ptr(),
+                                          self.sq_ws.data_ptr(), st), "panel fold")
+            _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p1.ref, self.RtW.data_ptr(), self.k,
+                                          self.out_scale, 1 if lean else 0, None, None, st),
+                       "panel fold")
+        if side is not None:
+            torch.cuda.current_stream().wait_event(self._ev_join)
 
 
 def best_sweep_plan(obs: ObservationSet, k: int, *, want_r: bool = True, out_scale: float = 1.0,

@@ -34,6 +34,7 @@ def _check(plan, om, wt, ht, k):
         assert torch.equal(a, b)  # bitwise run to run
 
 
+@pytest.mark.parametrize("cold", ["pieces", "gather"])
 @pytest.mark.parametrize("k", [40, 30, 32, 64])
 @pytest.mark.parametrize("cfg", [
     dict(),                                              # defaults
@@ -41,7 +42,7 @@ def _check(plan, om, wt, ht, k):
     dict(lmin=10 ** 9),                                   # nothing hot: all entries cold
     dict(lmin=1, max_panels=10 ** 6, min_panel_entries=1),  # every entry hot
 ])
-def test_hybrid_sweep_vs_oracle(k, cfg):
+def test_hybrid_sweep_vs_oracle(k, cfg, cold):
     from paper_2204_14067_b200.panel import HybridSweepPlan
     m, n, r, c, v = synth.generate("c3", scale=0.03, seed=200 + k)
     m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
@@ -51,7 +52,8 @@ def test_hybrid_sweep_vs_oracle(k, cfg):
     obs = D.ObservationSet.from_coo(m, n, r, c, v32, dtype=torch.float32)
     wt = torch.as_tensor(w).float().cuda()
     ht = torch.as_tensor(h).float().cuda()
-    plan = HybridSweepPlan(obs, k, **cfg)
+    plan = HybridSweepPlan(obs, k, cold=cold, **cfg)
+    assert plan.cold == (cold if k != 64 else "gather")
     if cfg.get("lmin", 0) >= 10 ** 9:
         assert plan.stats["csr_hot"] == 0 and plan.stats["csc_hot"] == 0
     if cfg.get("max_panels", 0) >= 10 ** 6:
@@ -76,7 +78,8 @@ def test_hybrid_sweep_small_and_ragged():
     w, h = synth.sweep_factors(m, n, k, seed=3)
     wt = torch.as_tensor(w).float().cuda()
     ht = torch.as_tensor(h).float().cuda()
-    for cfg in (dict(lmin=1, min_panel_entries=1), dict(lmin=2, lmax=3, min_panel_entries=1)):
+    for cfg in (dict(lmin=1, min_panel_entries=1), dict(lmin=2, lmax=3, min_panel_entries=1),
+                dict(lmin=4, lmax=9, min_panel_entries=1, cold="gather")):
         plan = HybridSweepPlan(obs, k, **cfg)
         assert plan.stats["csr_hot"] > 0
         _check(plan, om, wt, ht, k)

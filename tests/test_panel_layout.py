@@ -80,6 +80,73 @@ def test_panel_layout_replay(cfg):
     assert np.abs(rhot[hp] - Rfull[ho]).max() < 1e-12
 
 
+@pytest.mark.parametrize("cfg", [
+    dict(PR=16, lmin=3, lmax=21, max_panels=6, min_panel_entries=10),
+    dict(PR=8, lmin=10 ** 6, lmax=7, max_panels=3, min_panel_entries=1),     # everything cold
+])
+def test_panel_layout_cold_pieces_replay(cfg):
+    """With cold_pieces the cold entries are pieces too (global row ids in
+    128-byte record blocks) and every output row is the fold of its slots."""
+    m, n, k = 60, 300, 40
+    rng, rows, cols, vals = _case(1, m, n, 0.5, 0.4)
+    nnz = len(rows)
+    lay = types.SimpleNamespace(nnz=nnz, nrows=m, ncols=n, idx=torch.tensor(cols, dtype=torch.int32),
+                                row_of=torch.tensor(rows, dtype=torch.int32))
+    PR = cfg.pop("PR")
+    pp = panel._PanelPass(lay, torch.tensor(vals), m, n, PR, k, 0, want_r=False, want_sq=True,
+                          cold_pieces=True, direct=True, **cfg)
+    W = rng.standard_normal((m, k))
+    H = rng.standard_normal((n, k))
+    po = np.zeros((pp.n_slots, k))
+    seen = np.zeros(pp.n_slots, int)
+    ids = pp.panel_ids.numpy()
+    recs = pp.recs.numpy()
+    loc16 = recs.view(np.int16).reshape(-1, 48)
+    for _, p, a, b in pp.plist.numpy():
+        prow = ids[p * PR:(p + 1) * PR]
+        for row, blk0, ln, slot in pp.pieces.numpy()[a:b]:
+            seen[slot] += 1
+            for e in range(ln):
+                blk, off = blk0 + e // 16, e % 16
+                g = prow[loc16[blk, off]]
+                a_e = float(recs[blk, 8 + off:9 + off].view(np.float32)[0])
+                po[slot] += (float(W[row] @ H[g]) - a_e) * H[g]
+    crecs = pp.cold_recs.numpy()
+    rcold = np.zeros((pp.n_cold_blocks + 2) * 16)
+    cp = pp.cold_pieces.numpy()[:pp.n_cold_pieces]
+    assert np.all(np.diff(cp[:, 2] & 0x3fffffff) <= 0)
+    RH = np.zeros((m, k))
+    ndirect = 0
+    for row, blk0, ln, slot in cp:
+        is_direct = (ln >> 30) != 0
+        ln &= 0x3fffffff
+        ndirect += is_direct
+        assert 1 <= ln <= cfg["lmax"]
+        seen[slot] += 1
+        for e in range(ln):
+            blk, off = blk0 + e // 16, e % 16
+            g = crecs[blk, off]
+            a_e = float(crecs[blk, 16 + off:17 + off].view(np.float32)[0])
+            r = float(W[row] @ H[g]) - a_e
+            rcold[blk * 16 + off] = r
+            if is_direct:
+                RH[row] += r * H[g]           # the piece writes its row itself
+            else:
+                po[slot] += r * H[g]
+    assert np.all(seen == 1) and ndirect == pp.n_direct
+    fr, fb, fc = pp.frows.numpy(), pp.fbeg.numpy(), pp.fcnt.numpy()
+    for f, row in enumerate(fr):
+        assert not RH[row].any()              # direct rows are not folded
+        RH[row] += po[fb[f]:fb[f] + fc[f]].sum(0)
+    Rfull = (W[rows] * H[cols]).sum(1) - vals.astype(np.float64)
+    RHref = np.zeros((m, k))
+    np.add.at(RHref, rows, Rfull[:, None] * H[cols])
+    assert np.abs(RH - RHref).max() < 1e-11
+    co, cpos = pp.cold_orig.numpy(), pp.cold_pos.numpy()
+    assert len(co) + pp.n_hot == nnz
+    assert np.abs(rcold[cpos] - Rfull[co]).max() < 1e-12
+
+
 def test_panel_layout_no_hot_entries():
     m, n, k = 10, 40, 40
     rng, rows, cols, vals = _case(3, m, n, 0.3, 0.0)

@@ -83,6 +83,11 @@ st = _lib.stream_ptr()
 
 
 def cold():
+    if hyb.cold == "pieces":
+        _lib.check(lib.mfg_cold_sweep(hyb.ld, hyb.p0.cold_ref, hyb.p1.cold_ref, wd.data_ptr(), hd.data_ptr(),
+                                      hyb.RH.data_ptr(), hyb.RtW.data_ptr(), 1.0,
+                                      hyb.cold_counters.data_ptr(), st), "cold")
+        return
     _lib.check(lib.mfg_sweep_sharded(_lib.MFG_F32, 0, hyb.cold_csr.ref, hyb.cold_csc.ref, k,
                hyb.cold_vals.data_ptr(), hyb.cold_vals_csc.data_ptr(), wd.data_ptr(), wd.data_ptr(),
                hyb.ld, hd.data_ptr(), hd.data_ptr(), hyb.ld, hyb._rcold.data_ptr(), hyb.RH.data_ptr(),
@@ -105,8 +110,8 @@ def pan():
 
 
 def fold():
-    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p0.ref, hyb.RH.data_ptr(), k, 1.0, hyb.sums.data_ptr(), hyb.sq_ws.data_ptr(), st), "f")
-    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p1.ref, hyb.RtW.data_ptr(), k, 1.0, None, None, st), "f")
+    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p0.ref, hyb.RH.data_ptr(), k, 1.0, 0, hyb.sums.data_ptr(), hyb.sq_ws.data_ptr(), st), "f")
+    _lib.check(lib.mfg_panel_fold(hyb.ld, k, hyb.p1.ref, hyb.RtW.data_ptr(), k, 1.0, 0, None, None, st), "f")
 
 
 def rg():

@@ -2,7 +2,8 @@
 export PYTHONDONTWRITEBYTECODE=1
 export MFG_SYNTH_CACHE=/tmp/synth
 tag=${TAG:-r2r}
-for cfg in "96 60000 8 256" "64 100000 16 256" "48 100000 8 256" "64 100000 8 511" "128 40000 12 256"; do
+IFS=";" read -ra CF <<< "${CFGS:-64 100000 8 256;64 100000 12 256;32 100000 16 256;48 100000 16 256;48 100000 24 256;64 100000 16 511}"
+for cfg in "${CF[@]}"; do
   set -- $cfg
   echo "== MAXP=$1 MINE=$2 LMIN=$3 LMAX=$4"
   MFG_PANEL_MAXP=$1 MFG_PANEL_MINE=$2 MFG_PANEL_LMIN=$3 MFG_PANEL_LMAX=$4 timeout 300 python tools/panel_probe.py c4 2>&1 | tail -2
