@@ -563,8 +563,11 @@ def main():
                    "timing": "per-step CUDA events, CUDA-graph replay of the sweep",
                    "parallelism": (f"{world} independent instances (one per GPU)" if world > 1
                                    else "1 GPU"),
-                   "sweep_plan": (dict(kind="hybrid: hot entries from shared-memory panels (k_panel), "
-                                       "cold entries through the gather kernel (k_sweep_g8f)",
+                   "sweep_plan": (dict(kind="hybrid: hot entries from shared-memory panels (k_panel4), "
+                                       "cold entries as pieces on global loads (k_cold4)"
+                                       if getattr(plan, "cold", "") == "pieces" else
+                                       "hybrid: hot entries from shared-memory panels, cold entries "
+                                       "through the gather kernel (k_sweep_g8f)",
                                        **plan.stats) if hybrid else {"kind": "gather (k_sweep_g8f)"}),
                    "plan_trial_ms": getattr(plan, "trial_ms", None),
                    "plan_seconds": round(t_plan, 3)},
@@ -574,8 +577,8 @@ def main():
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("one sweep = k_sweep_g8f (cold entries) + k_panel + k_panel_fold x4 "
-                                "+ k_panel_sq + k_gather4_f32; k_panel is the longest"
+                     "kernel": ("one sweep = k_cold4 (cold entries) + k_panel4 (hot entries, the longest) "
+                                "+ k_panel_fold x3-4 + k_panel_sq + k_gather4_f32 + 2 k_dot (norms)"
                                 if hybrid else "k_sweep_g8f (fused CSR+CSC pass)"),
                      "bytes_per_launch": kb, "avg_launch_us": kern_ms * 1e3,
                      "peak_source": peak_src,

@@ -54,13 +54,19 @@ k_dot(int64_t n, const T* __restrict__ x, const T* __restrict__ y, double* __res
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
+    // the last block adds the block partials: each thread a fixed strided
+    // subset, then the fixed block tree (deterministic; a single thread
+    // walking up to 2368 partials took ~70 us)
     __threadfence();
     const volatile double* b = bp;
     double t = 0.0;
-    for (unsigned int i = 0; i < gridDim.x; ++i) t += b[i];
-    *out = t;
-    *counter = 0u;
+    for (unsigned int i = threadIdx.x; i < gridDim.x; i += 256) t += b[i];
+    const double tot = block_sum<256>(t, sm);
+    if (threadIdx.x == 0) {
+      *out = tot;
+      *counter = 0u;
+    }
   }
 }
 

@@ -481,10 +481,19 @@ class HybridSweepPlan:
         else:
             self._wd[:, :k].copy_(w_host, non_blocking=True)
             self._hd[:, :k].copy_(h_host, non_blocking=True)
-        self.run(self._wd, self._hd)
+        # the D2H of [sums | RH | RtW] does not wait for R (side stream)
+        pending = self._enqueue(self._wd, self._hd)
         self._host.copy_(self._out, non_blocking=True)
+        if pending:
+            torch.cuda.current_stream().wait_event(self._ev_join)
 
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
+        if self._enqueue(w, h):
+            torch.cuda.current_stream().wait_event(self._ev_join)
+
+    def _enqueue(self, w: torch.Tensor, h: torch.Tensor) -> bool:
+        """Enqueue one sweep; True when the R gather runs on the side stream and
+        the caller still has to wait for ``_ev_join``."""
         lib = _lib.lib()
         st = _lib.stream_ptr()
         if int(w.stride(0)) != self.ld or int(h.stride(0)) != self.ld:
@@ -535,8 +544,7 @@ class HybridSweepPlan:
             _lib.check(lib.mfg_panel_fold(self.ld, self.k, self.p1.ref, self.RtW.data_ptr(), self.k,
                                           self.out_scale, 1 if lean else 0, None, None, st),
                        "panel fold")
-        if side is not None:
-            torch.cuda.current_stream().wait_event(self._ev_join)
+        return side is not None
 
 
 def best_sweep_plan(obs: ObservationSet, k: int, *, want_r: bool = True, out_scale: float = 1.0,

@@ -129,3 +129,41 @@ def test_hybrid_run_host_and_plan_choice():
         p.run(p.pad(wt), p.pad(ht))
         assert torch.allclose(p.RH.cpu(), ref[1], rtol=0, atol=2e-4 * float(ref[1].abs().max()))
         assert float(p.sums[0]) == pytest.approx(float(ref[0][0]), rel=1e-6)
+
+
+@pytest.mark.parametrize("cold", ["pieces", "gather"])
+def test_hybrid_out_scale_and_no_r(cold):
+    """out_scale multiplies R.H and R^T.W on every path (folded rows, rows a
+    single cold piece writes directly, the gather kernel's rows); want_r=False
+    skips the residual output."""
+    from paper_2204_14067_b200.panel import HybridSweepPlan
+    k = 40
+    m, n, r, c, v = synth.generate("c3", scale=0.02, seed=91)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    v32 = v.astype(np.float32).astype(np.float64)
+    om = orc.from_coo(m, n, r, c, v32)
+    obs = D.ObservationSet.from_coo(m, n, r, c, v32, dtype=torch.float32)
+    w, h = synth.sweep_factors(m, n, k, seed=9)
+    wt = torch.as_tensor(w).float().cuda()
+    ht = torch.as_tensor(h).float().cuda()
+    plan = HybridSweepPlan(obs, k, want_r=False, out_scale=2.0, cold=cold)
+    assert plan.R is None
+    if cold == "pieces":
+        assert plan.p1.n_direct > 0          # light columns: one cold piece each
+    plan.run(plan.pad(wt), plan.pad(ht))
+    rr, rh, rtw, sq, w2, h2 = orc.sweep(om, _np(wt), _np(ht))
+    sc = lambda a: max(1.0, np.abs(a).max())  # noqa: E731
+    assert np.max(np.abs(_np(plan.RH) - 2.0 * rh)) <= 4e-4 * sc(rh)
+    assert np.max(np.abs(_np(plan.RtW) - 2.0 * rtw)) <= 4e-4 * sc(rtw)
+    sums = plan.sums.cpu().numpy()
+    assert sums[0] == pytest.approx(sq, rel=2e-4)
+    assert sums[1] == pytest.approx(w2, rel=1e-12) and sums[2] == pytest.approx(h2, rel=1e-12)
+    # a second sweep with other factors reuses the plan (outputs fully rewritten)
+    w3, h3 = synth.sweep_factors(m, n, k, seed=10)
+    wt3 = torch.as_tensor(w3).float().cuda()
+    ht3 = torch.as_tensor(h3).float().cuda()
+    plan.run(plan.pad(wt3), plan.pad(ht3))
+    _, rh3, rtw3, sq3, _, _ = orc.sweep(om, _np(wt3), _np(ht3))
+    assert np.max(np.abs(_np(plan.RH) - 2.0 * rh3)) <= 4e-4 * sc(rh3)
+    assert np.max(np.abs(_np(plan.RtW) - 2.0 * rtw3)) <= 4e-4 * sc(rtw3)
+    assert plan.sums.cpu().numpy()[0] == pytest.approx(sq3, rel=2e-4)
