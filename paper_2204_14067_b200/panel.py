@@ -353,6 +353,19 @@ class HybridSweepPlan:
             self.plist = torch.zeros((1, 4), dtype=torch.int32, device=dev.device)
             start = torch.zeros(nctas, dtype=torch.long)
         self.cta_start = start.to(torch.int32).to(dev.device)
+        # per-pass lists for the end-to-end path (CSC pass first, so that the D2H of
+        # R^T.W overlaps the CSR pass): their own CTA starts and tickets
+        self._pass_lists = []
+        for pp in (self.p0, self.p1):
+            nl = int(pp.plist.shape[0])
+            if nl:
+                ed = torch.cumsum(pp.plist_entries.double(), 0)
+                at = (torch.arange(nctas, dtype=torch.float64) + 0.5) * float(ed[-1]) / nctas
+                cs = torch.searchsorted(ed, at).clamp_(max=nl - 1).to(torch.int32).to(dev.device)
+            else:
+                cs = torch.zeros(nctas, dtype=torch.int32, device=dev.device)
+            self._pass_lists.append((nl, pp.plist.contiguous(), cs,
+                                     torch.zeros(nl + 2, dtype=torch.int32, device=dev.device)))
         nnz = obs.size
         self.want_r = want_r
         nh_pad = (self.p0.n_blocks + 2) * 16
@@ -395,6 +408,8 @@ class HybridSweepPlan:
         if lean:
             self.wsb = 1 << 16        # the two norms (mfg_dot)
             self.cold_counters = torch.zeros(4, dtype=torch.int32, device=dev.device)
+            # a pass's cold pieces alone: the other pass's struct with no pieces
+            self._no_cold = _lib.PanelPass(0, 0, 0, None, None, None, None, None, None, None, None, None)
         else:
             self.wsb = lib.mfg_sweep_workspace(self.cold_csr.ref, self.cold_csc.ref, self.k)
         self.ws = torch.zeros(self.wsb, dtype=torch.uint8, device=dev.device)
@@ -403,6 +418,9 @@ class HybridSweepPlan:
         self._side = torch.cuda.Stream(device=dev.device)
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
+        self._copy = torch.cuda.Stream(device=dev.device)
+        self._ev_csc = torch.cuda.Event()
+        self._ev_copy = torch.cuda.Event()
         self.stats = {
             "panel_rows": self.PR, "csr_panels": self.p0.n_panels, "csc_panels": self.p1.n_panels,
             "csr_hot": self.p0.n_hot, "csc_hot": self.p1.n_hot, "nnz": nnz,
@@ -481,11 +499,67 @@ class HybridSweepPlan:
         else:
             self._wd[:, :k].copy_(w_host, non_blocking=True)
             self._hd[:, :k].copy_(h_host, non_blocking=True)
+        cur = torch.cuda.current_stream()
+        if self.cold == "pieces":
+            # CSC pass first: the D2H of R^T.W (the large output) runs on a copy
+            # stream while the CSR pass computes
+            self._enqueue_pass(self._wd, self._hd, 1)
+            nb_head = 32 + self.RH.numel() * 4
+            self._ev_csc.record(cur)
+            self._copy.wait_event(self._ev_csc)
+            with torch.cuda.stream(self._copy):
+                self._host[nb_head:].copy_(self._out[nb_head:], non_blocking=True)
+                self._ev_copy.record(self._copy)
+            pending = self._enqueue_pass(self._wd, self._hd, 0)
+            self._host[:nb_head].copy_(self._out[:nb_head], non_blocking=True)
+            if pending:
+                cur.wait_event(self._ev_join)
+            cur.wait_event(self._ev_copy)
+            return
         # the D2H of [sums | RH | RtW] does not wait for R (side stream)
         pending = self._enqueue(self._wd, self._hd)
         self._host.copy_(self._out, non_blocking=True)
         if pending:
-            torch.cuda.current_stream().wait_event(self._ev_join)
+            cur.wait_event(self._ev_join)
+
+    def _enqueue_pass(self, w: torch.Tensor, h: torch.Tensor, ps: int) -> bool:
+        """One pass of the sweep (cold="pieces" plans): 0 = CSR (R, R.H, sum r^2,
+        the norms), 1 = CSC (R^T.W). True when the R gather is pending on the
+        side stream."""
+        lib = _lib.lib()
+        st = _lib.stream_ptr()
+        pp = self.p0 if ps == 0 else self.p1
+        none = ctypes.byref(self._no_cold)
+        if ps == 0:
+            self.sums[0:1].zero_()
+            for x, o in ((w, 1), (h, 2)):
+                _lib.check(lib.mfg_dot(_lib.MFG_F32, x.shape[0] * self.ld, x.data_ptr(), x.data_ptr(),
+                                       self.sums.data_ptr() + 8 * o, self.ws.data_ptr(), self.wsb, st),
+                           "norm")
+        _lib.check(lib.mfg_cold_sweep(self.ld, pp.cold_ref if ps == 0 else none,
+                                      pp.cold_ref if ps == 1 else none, w.data_ptr(), h.data_ptr(),
+                                      self.RH.data_ptr(), self.RtW.data_ptr(), self.out_scale,
+                                      self.cold_counters.data_ptr(), st), "cold sweep")
+        nl, plist, cs, cnt = self._pass_lists[ps]
+        if nl:
+            _lib.check(lib.mfg_panel_sweep(self.ld, nl, plist.data_ptr(), cs.data_ptr(), self.p0.ref,
+                                           self.p1.ref, w.data_ptr(), h.data_ptr(), cnt.data_ptr(), st),
+                       "panel sweep")
+        pending = False
+        if ps == 0 and self.want_r:
+            cur = torch.cuda.current_stream()
+            self._ev_fork.record(cur)
+            self._side.wait_event(self._ev_fork)
+            _lib.check(lib.mfg_gather(_lib.MFG_F32, self.obs.size, self._rsrc.data_ptr(),
+                                      self._rcat.data_ptr(), self.R.data_ptr(), self._side.cuda_stream),
+                       "R gather")
+            self._ev_join.record(self._side)
+            pending = True
+        out = self.RH if ps == 0 else self.RtW
+        _lib.check(lib.mfg_panel_fold(self.ld, self.k, pp.ref, out.data_ptr(), self.k, self.out_scale, 1,
+                                      self.sums.data_ptr() if ps == 0 else None,
+                                      self.sq_ws.data_ptr() if ps == 0 else None, st), "panel fold")
+        return pending
 
     def run(self, w: torch.Tensor, h: torch.Tensor) -> None:
         if self._enqueue(w, h):
