@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(const PanelArgs A) {
   const int t_sh = (ei & 1) * 16;       // ... and its half
   const bool b2 = (q & 4) != 0, b1 = (q & 2) != 0, even = (q & 1) == 0;
   const int gb = lane & 24;
+  int cur_key = -1;
   int li = A.cta_start[blockIdx.x];
   for (int step = 0; step < A.n_list; ++step, li = li + 1 == A.n_list ? 0 : li + 1) {
     const int4 it = A.plist[li];        // {pass, panel, first piece, end piece}
@@ -145,7 +146,9 @@ __global__ void __launch_bounds__(kPT, 1) k_panel(const PanelArgs A) {
     __syncthreads();
     if (s_left <= 0) continue;          // this panel's pieces are all taken
     const PanelPass& P = A.p[it.x];
-    {
+    const int key = it.x * 65536 + it.y;
+    if (key != cur_key) {               // consecutive elements may share a panel (column chunks)
+      cur_key = key;
       const int32_t* ids = P.panel_ids + (size_t)it.y * A.PR;
       const int total = A.PR * KC;
       for (int c = tid; c < total; c += kPT) {
@@ -363,6 +366,7 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
   const bool hi1 = (q & 2) != 0, odd = (q & 1) != 0;
   const bool gpar = (g & 1) != 0;       // odd groups load their tails in the opposite order
   const int gb = lane & 28;
+  int cur_key = -1;
   int li = A.cta_start[blockIdx.x];
   for (int step = 0; step < A.n_list; ++step, li = li + 1 == A.n_list ? 0 : li + 1) {
     const int4 it = A.plist[li];        // {pass, panel, first piece, end piece}
@@ -372,7 +376,9 @@ __global__ void __launch_bounds__(kPT4, 1) k_panel4(const PanelArgs A) {
     __syncthreads();
     if (s_left <= 0) continue;          // this panel's pieces are all taken
     const PanelPass& P = A.p[it.x];
-    {
+    const int key = it.x * 65536 + it.y;
+    if (key != cur_key) {               // consecutive elements may share a panel (column chunks)
+      cur_key = key;
       const int32_t* ids = P.panel_ids + (size_t)it.y * A.PR;
       const int total = A.PR * KC;
       for (int c = tid; c < total; c += kPT4) {

@@ -68,8 +68,18 @@ class _PanelPass:
     def __init__(self, lay: _LayoutBuffers, vals: torch.Tensor, n_self: int, n_gath: int, PR: int,
                  ld: int, pass_id: int, *, lmin: int, lmax: int,
                  max_panels: int, min_panel_entries: int, want_r: bool, want_sq: bool,
-                 cold_pieces: bool = False, direct: bool = False):
+                 cold_pieces: bool = False, direct: bool = False, nchunks: int = 1):
         dev = vals.device
+        nchunks = max(1, min(int(nchunks), max(n_self, 1)))
+        self.nchunks = nchunks
+        # self rows in nchunks contiguous ranges (the end-to-end path moves and
+        # processes the CSC pass's self factor H chunk by chunk)
+        self.chunk_rows = [(c * n_self + nchunks - 1) // nchunks for c in range(nchunks + 1)]
+        bounds = torch.tensor(self.chunk_rows[1:], device=dev)
+
+        def chunk_of(rows_t):
+            return torch.bucketize(rows_t, bounds, right=True)
+
         nnz = lay.nnz
         idx = lay.idx[:nnz].long()
         row_of = lay.row_of[:nnz].long()
@@ -225,32 +235,55 @@ class _PanelPass:
         self.fbeg = fbeg[o_lh].to(torch.int32)
         self.fcnt = counts[o_lh].to(torch.int32)
         # piece table: per panel by decreasing length
-        o_pl = torch.argsort(span * (lmax + 1) + (lmax - slen), stable=True)
+        span2 = span * nchunks + chunk_of(srow)             # (panel, chunk of the self row)
+        o_pl = torch.argsort(span2 * (lmax + 1) + (lmax - slen), stable=True)
         pieces = torch.stack([srow[o_pl], bstart[o_pl], slen[o_pl], slot[:ns][o_pl]], dim=1).to(torch.int32)
         self.pieces = pieces.contiguous() if ns else torch.zeros((1, 4), dtype=torch.int32, device=dev)
         self.n_pieces = ns
         self.n_slots = nsa
         if cold_pieces:
-            o_c = torch.argsort(lmax - slen_c, stable=True)
+            chunk_c = chunk_of(srow_c)
+            o_c = torch.argsort(chunk_c * (lmax + 1) + (lmax - slen_c), stable=True)
+            cc_cnt = torch.bincount(chunk_c, minlength=nchunks).cpu().tolist() if nsc else [0] * nchunks
+            self.cold_chunk_ptr = [0]
+            for x in cc_cnt:
+                self.cold_chunk_ptr.append(self.cold_chunk_ptr[-1] + int(x))
             lenf = slen_c if direct_c is None else slen_c + direct_c.long() * (1 << 30)
             self.n_direct = 0 if direct_c is None else int(direct_c.sum().item())
             cp = torch.stack([srow_c[o_c], bstart_c[o_c], lenf[o_c], slot[ns:][o_c]], dim=1).to(torch.int32)
             self.cold_pieces = cp.contiguous() if nsc else torch.zeros((1, 4), dtype=torch.int32, device=dev)
             self.n_cold_pieces = nsc
-        # panel list: {pass, panel, first piece, end piece} + entries per element
-        span_s = span[o_pl]
+        # panel list: {pass, panel, first piece, end piece}, one element per
+        # (panel, chunk), + entries and chunk of each element
+        span_s = span2[o_pl]
         if ns:
             f3 = torch.ones(ns, dtype=torch.bool, device=dev)
             f3[1:] = span_s[1:] != span_s[:-1]
             ist = torch.nonzero(f3).flatten()
             iend = torch.cat([ist[1:], torch.tensor([ns], device=dev)])
-            self.plist = torch.stack([torch.full_like(ist, pass_id), span_s[ist], ist, iend],
+            self.plist = torch.stack([torch.full_like(ist, pass_id), span_s[ist] // nchunks, ist, iend],
                                      dim=1).to(torch.int32)
             cum = torch.cat([torch.zeros(1, dtype=torch.long, device=dev), torch.cumsum(slen[o_pl], 0)])
             self.plist_entries = (cum[iend] - cum[ist]).cpu()
+            self.plist_chunk = (span_s[ist] % nchunks).cpu()
         else:
             self.plist = torch.zeros((0, 4), dtype=torch.int32, device=dev)
             self.plist_entries = torch.zeros(0, dtype=torch.long)
+            self.plist_chunk = torch.zeros(0, dtype=torch.long)
+        # fold lists per chunk (light rows, then heavy rows, inside each chunk)
+        if nchunks > 1:
+            fch = chunk_of(frows)
+            o_cf = torch.argsort(fch * 2 + (counts > 32).long(), stable=True)
+            self.cf_rows = frows[o_cf].to(torch.int32)
+            self.cf_beg = fbeg[o_cf].to(torch.int32)
+            self.cf_cnt = counts[o_cf].to(torch.int32)
+            nr = torch.bincount(fch, minlength=nchunks).cpu().tolist() if frows.numel() else [0] * nchunks
+            nlt = (torch.bincount(fch[counts <= 32], minlength=nchunks).cpu().tolist()
+                   if frows.numel() else [0] * nchunks)
+            self.cf_info, off = [], 0
+            for c in range(nchunks):
+                self.cf_info.append((off, int(nr[c]), int(nlt[c])))
+                off += int(nr[c])
         # outputs / scratch (slots are shared by the hot and the cold pieces)
         self.r_hot = torch.zeros((n_blocks + 2) * 16, dtype=torch.float32, device=dev) if want_r else None
         self.piece_out = torch.empty((max(nsa, 1), ld), dtype=torch.float32, device=dev)
@@ -272,6 +305,24 @@ class _PanelPass:
     @property
     def cold_ref(self):
         return ctypes.byref(self.cc)
+
+    def chunk_structs(self):
+        """Per chunk: (fold struct, cold-piece struct) -- copies of ``c`` / ``cc``
+        restricted to the chunk's self rows."""
+        out = []
+        for c in range(self.nchunks):
+            off, nr, nlt = self.cf_info[c]
+            f = _lib.PanelPass.from_buffer_copy(self.c)
+            f.n_frows, f.n_light = nr, nlt
+            f.frows = self.cf_rows.data_ptr() + 4 * off
+            f.fbeg = self.cf_beg.data_ptr() + 4 * off
+            f.fcnt = self.cf_cnt.data_ptr() + 4 * off
+            g = _lib.PanelPass.from_buffer_copy(self.cc)
+            c0, c1 = self.cold_chunk_ptr[c], self.cold_chunk_ptr[c + 1]
+            g.n_pieces = c1 - c0
+            g.pieces = self.cold_pieces.data_ptr() + 16 * c0
+            out.append((f, g))
+        return out
 
 
 def _cold_layout(lay: _LayoutBuffers, vals: torch.Tensor, cold: torch.Tensor):
@@ -337,8 +388,11 @@ class HybridSweepPlan:
                   cold_pieces=lean, direct=lean and self.ld == self.k)
         self.p0 = _PanelPass(dev.csr, dev.vals, obs.m, obs.n, self.PR, self.ld, 0, want_r=False,
                              want_sq=True, **kw)
+        # the CSC pass in column chunks: the end-to-end path moves H, computes and
+        # returns R^T.W chunk by chunk (cold="pieces" plans)
+        self.nchunks = int(env("MFG_PANEL_CHUNKS", 4)) if lean else 1
         self.p1 = _PanelPass(dev.csc, dev.vals_csc, obs.n, obs.m, self.PR, self.ld, 1,
-                             want_r=False, want_sq=False, **kw)
+                             want_r=False, want_sq=False, nchunks=self.nchunks, **kw)
         # one list over both passes; the CSC pass's piece indices are its own
         self.plist = torch.cat([self.p0.plist, self.p1.plist], 0).contiguous()
         self.n_list = int(self.plist.shape[0])
@@ -366,6 +420,22 @@ class HybridSweepPlan:
                 cs = torch.zeros(nctas, dtype=torch.int32, device=dev.device)
             self._pass_lists.append((nl, pp.plist.contiguous(), cs,
                                      torch.zeros(nl + 2, dtype=torch.int32, device=dev.device)))
+        self._chunk_lists = []
+        if self.p1.nchunks > 1:
+            for c in range(self.p1.nchunks):
+                sel = torch.nonzero(self.p1.plist_chunk == c).flatten()
+                nl = int(sel.numel())
+                if nl:
+                    pl = self.p1.plist[sel.to(dev.device)].contiguous()
+                    ed = torch.cumsum(self.p1.plist_entries[sel].double(), 0)
+                    at = (torch.arange(nctas, dtype=torch.float64) + 0.5) * float(ed[-1]) / nctas
+                    cs = torch.searchsorted(ed, at).clamp_(max=nl - 1).to(torch.int32).to(dev.device)
+                else:
+                    pl = torch.zeros((1, 4), dtype=torch.int32, device=dev.device)
+                    cs = torch.zeros(nctas, dtype=torch.int32, device=dev.device)
+                self._chunk_lists.append((nl, pl, cs, torch.zeros(nl + 2, dtype=torch.int32,
+                                                                  device=dev.device)))
+            self._chunk_structs = self.p1.chunk_structs()
         nnz = obs.size
         self.want_r = want_r
         nh_pad = (self.p0.n_blocks + 2) * 16
@@ -421,6 +491,11 @@ class HybridSweepPlan:
         self._copy = torch.cuda.Stream(device=dev.device)
         self._ev_csc = torch.cuda.Event()
         self._ev_copy = torch.cuda.Event()
+        self._cin = torch.cuda.Stream(device=dev.device)
+        self._ev_start = torch.cuda.Event()
+        self._ev_w = torch.cuda.Event()
+        self._ev_h = [torch.cuda.Event() for _ in range(max(self.nchunks, 1))]
+        self._ev_f = [torch.cuda.Event() for _ in range(max(self.nchunks, 1))]
         self.stats = {
             "panel_rows": self.PR, "csr_panels": self.p0.n_panels, "csc_panels": self.p1.n_panels,
             "csr_hot": self.p0.n_hot, "csc_hot": self.p1.n_hot, "nnz": nnz,
@@ -491,6 +566,9 @@ class HybridSweepPlan:
 
     def _host_call(self, w_host, h_host):
         m, n, k, ld = self.obs.m, self.obs.n, self.k, self.ld
+        if self.cold == "pieces" and self._chunk_lists:
+            self._host_call_chunked(w_host, h_host)
+            return
         adjacent = (ld == k and h_host.data_ptr() == w_host.data_ptr() + m * k * 4
                     and w_host.untyped_storage().data_ptr() == h_host.untyped_storage().data_ptr())
         if adjacent:
@@ -521,6 +599,57 @@ class HybridSweepPlan:
         self._host.copy_(self._out, non_blocking=True)
         if pending:
             cur.wait_event(self._ev_join)
+
+    def _host_call_chunked(self, w_host, h_host):
+        """The end-to-end step as a pipeline over column chunks: H moves to the
+        device chunk by chunk on a copy-in stream; as soon as a chunk of H has
+        arrived the CSC pass runs on its columns (cold pieces, panel pieces,
+        fold) and the chunk's rows of R^T.W return on a copy-out stream; the
+        CSR pass (which gathers all of H) follows the last chunk."""
+        lib = _lib.lib()
+        m, n, k, ld = self.obs.m, self.obs.n, self.k, self.ld
+        cur = torch.cuda.current_stream()
+        cin, cout = self._cin, self._copy
+        nc = self.p1.nchunks
+        cr = self.p1.chunk_rows
+        self._ev_start.record(cur)
+        cin.wait_event(self._ev_start)
+        cout.wait_event(self._ev_start)
+        with torch.cuda.stream(cin):
+            self._wd[:, :k].copy_(w_host, non_blocking=True)
+            self._ev_w.record(cin)
+            for c in range(nc):
+                self._hd[cr[c]:cr[c + 1], :k].copy_(h_host[cr[c]:cr[c + 1]], non_blocking=True)
+                self._ev_h[c].record(cin)
+        cur.wait_event(self._ev_w)
+        st = cur.cuda_stream
+        none = ctypes.byref(self._no_cold)
+        nb_head = 32 + self.RH.numel() * 4
+        for c in range(nc):
+            cur.wait_event(self._ev_h[c])
+            fold_c, cold_c = self._chunk_structs[c]
+            _lib.check(lib.mfg_cold_sweep(ld, none, ctypes.byref(cold_c), self._wd.data_ptr(),
+                                          self._hd.data_ptr(), self.RH.data_ptr(), self.RtW.data_ptr(),
+                                          self.out_scale, self.cold_counters.data_ptr(), st),
+                       "cold sweep")
+            nl, plist, cs, cnt = self._chunk_lists[c]
+            if nl:
+                _lib.check(lib.mfg_panel_sweep(ld, nl, plist.data_ptr(), cs.data_ptr(), self.p0.ref,
+                                               self.p1.ref, self._wd.data_ptr(), self._hd.data_ptr(),
+                                               cnt.data_ptr(), st), "panel sweep")
+            _lib.check(lib.mfg_panel_fold(ld, k, ctypes.byref(fold_c), self.RtW.data_ptr(), k,
+                                          self.out_scale, 1, None, None, st), "panel fold")
+            self._ev_f[c].record(cur)
+            cout.wait_event(self._ev_f[c])
+            b0, b1 = nb_head + cr[c] * k * 4, nb_head + cr[c + 1] * k * 4
+            with torch.cuda.stream(cout):
+                self._host[b0:b1].copy_(self._out[b0:b1], non_blocking=True)
+        self._ev_copy.record(cout)
+        pending = self._enqueue_pass(self._wd, self._hd, 0)
+        self._host[:nb_head].copy_(self._out[:nb_head], non_blocking=True)
+        if pending:
+            cur.wait_event(self._ev_join)
+        cur.wait_event(self._ev_copy)
 
     def _enqueue_pass(self, w: torch.Tensor, h: torch.Tensor, ps: int) -> bool:
         """One pass of the sweep (cold="pieces" plans): 0 = CSR (R, R.H, sum r^2,

@@ -156,3 +156,41 @@ def test_panel_layout_no_hot_entries():
                           min_panel_entries=1, want_r=False, want_sq=False)
     assert pp.n_hot == 0 and pp.n_pieces == 0 and pp.plist.shape[0] == 0
     assert bool(pp.cold_mask.all())
+
+
+def test_panel_layout_chunks():
+    """nchunks > 1 (the end-to-end path's CSC pass): every list element, cold
+    piece range and fold range stays inside one contiguous range of self rows."""
+    m, n, k = 60, 300, 40
+    rng, rows, cols, vals = _case(2, m, n, 0.5, 0.4)
+    lay = types.SimpleNamespace(nnz=len(rows), nrows=m, ncols=n, idx=torch.tensor(cols, dtype=torch.int32),
+                                row_of=torch.tensor(rows, dtype=torch.int32))
+    nc = 3
+    pp = panel._PanelPass(lay, torch.tensor(vals), m, n, 16, k, 1, lmin=3, lmax=21, max_panels=6,
+                          min_panel_entries=10, want_r=False, want_sq=False, cold_pieces=True,
+                          direct=True, nchunks=nc)
+    cr = pp.chunk_rows
+    assert cr[0] == 0 and cr[-1] == m and len(cr) == nc + 1
+    pieces = pp.pieces.numpy()
+    panels = []
+    for (_, p, a, b), c in zip(pp.plist.numpy(), pp.plist_chunk.numpy()):
+        panels.append(p)
+        r = pieces[a:b, 0]
+        assert np.all((r >= cr[c]) & (r < cr[c + 1]))
+        assert np.all(np.diff(pieces[a:b, 2]) <= 0)
+    assert panels == sorted(panels)            # panel-major: consecutive elements share a panel
+    cp = pp.cold_pieces.numpy()
+    ptr = pp.cold_chunk_ptr
+    assert ptr[0] == 0 and ptr[-1] == pp.n_cold_pieces
+    for c in range(nc):
+        r = cp[ptr[c]:ptr[c + 1], 0]
+        assert np.all((r >= cr[c]) & (r < cr[c + 1]))
+    tot = 0
+    for c, (off, nr, nlt) in enumerate(pp.cf_info):
+        r = pp.cf_rows.numpy()[off:off + nr]
+        cnt = pp.cf_cnt.numpy()[off:off + nr]
+        assert np.all((r >= cr[c]) & (r < cr[c + 1]))
+        assert np.all(cnt[:nlt] <= 32) and np.all(cnt[nlt:] > 32)
+        tot += nr
+    assert tot == pp.frows.numel()
+    assert sorted(pp.cf_rows.numpy().tolist()) == sorted(pp.frows.numpy().tolist())
