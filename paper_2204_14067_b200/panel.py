@@ -74,7 +74,16 @@ class _PanelPass:
         self.nchunks = nchunks
         # self rows in nchunks contiguous ranges (the end-to-end path moves and
         # processes the CSC pass's self factor H chunk by chunk)
-        self.chunk_rows = [(c * n_self + nchunks - 1) // nchunks for c in range(nchunks + 1)]
+        # chunk sizes shrink geometrically (ratio MFG_PANEL_CHUNK_RATIO): the last
+        # chunk's compute is not hidden behind a transfer, so it is the smallest
+        rho = float(os.environ.get("MFG_PANEL_CHUNK_RATIO", 0.7))
+        wts = [rho ** c for c in range(nchunks)]
+        acc, tot = 0.0, sum(wts)
+        self.chunk_rows = [0]
+        for c in range(nchunks):
+            acc += wts[c]
+            self.chunk_rows.append(n_self if c == nchunks - 1 else
+                                   max(self.chunk_rows[-1], min(n_self, int(round(n_self * acc / tot)))))
         bounds = torch.tensor(self.chunk_rows[1:], device=dev)
 
         def chunk_of(rows_t):
