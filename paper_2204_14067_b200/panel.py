@@ -42,6 +42,19 @@ def panel_ld(k: int, dtype) -> int:
     return ld if ld and _lib.lib().mfg_panel_rows(ld) > 0 else 0
 
 
+def _chunk_rows(n: int, nchunks: int, rho: float) -> list:
+    """Boundaries of nchunks contiguous row ranges of n rows whose sizes shrink
+    geometrically (ratio rho): the last chunk's work is not hidden behind a
+    transfer, so it is the smallest."""
+    nchunks = max(1, min(int(nchunks), max(n, 1)))
+    wts = [rho ** c for c in range(nchunks)]
+    acc, tot, out = 0.0, sum(wts), [0]
+    for c in range(nchunks):
+        acc += wts[c]
+        out.append(n if c == nchunks - 1 else max(out[-1], min(n, int(round(n * acc / tot)))))
+    return out
+
+
 def _cut(lens, prow, ppan, lmax, dev):
     """Cut pieces into sub-pieces of at most lmax entries (balanced lengths).
     Returns (srow, span, slen, cstart): self row, panel, length and first
@@ -68,42 +81,63 @@ class _PanelPass:
     def __init__(self, lay: _LayoutBuffers, vals: torch.Tensor, n_self: int, n_gath: int, PR: int,
                  ld: int, pass_id: int, *, lmin: int, lmax: int,
                  max_panels: int, min_panel_entries: int, want_r: bool, want_sq: bool,
-                 cold_pieces: bool = False, direct: bool = False, nchunks: int = 1):
+                 cold_pieces: bool = False, direct: bool = False, chunk_rows=None,
+                 chunk_by: str = "self"):
+        """``chunk_rows``: boundaries [0, .., n] of contiguous row ranges of one
+        factor (the end-to-end path moves that factor chunk by chunk).
+        ``chunk_by`` = "self": they cut this pass's self rows (the CSC pass and
+        H): every list element, cold piece and fold range lies in one chunk.
+        "gath": they cut the gathered table (the CSR pass and H): panels hold
+        rows of one chunk and a cold piece gathers from one chunk, so the work
+        that needs chunk c only needs chunk c."""
         dev = vals.device
-        nchunks = max(1, min(int(nchunks), max(n_self, 1)))
+        if chunk_rows is None or len(chunk_rows) < 3:
+            chunk_rows = [0, n_self if chunk_by == "self" else n_gath]
+        nchunks = len(chunk_rows) - 1
         self.nchunks = nchunks
-        # self rows in nchunks contiguous ranges (the end-to-end path moves and
-        # processes the CSC pass's self factor H chunk by chunk)
-        # chunk sizes shrink geometrically (ratio MFG_PANEL_CHUNK_RATIO): the last
-        # chunk's compute is not hidden behind a transfer, so it is the smallest
-        rho = float(os.environ.get("MFG_PANEL_CHUNK_RATIO", 0.7))
-        wts = [rho ** c for c in range(nchunks)]
-        acc, tot = 0.0, sum(wts)
-        self.chunk_rows = [0]
-        for c in range(nchunks):
-            acc += wts[c]
-            self.chunk_rows.append(n_self if c == nchunks - 1 else
-                                   max(self.chunk_rows[-1], min(n_self, int(round(n_self * acc / tot)))))
+        self.chunk_rows = list(chunk_rows)
+        self.chunk_by = chunk_by
         bounds = torch.tensor(self.chunk_rows[1:], device=dev)
 
         def chunk_of(rows_t):
-            return torch.bucketize(rows_t, bounds, right=True)
+            return torch.bucketize(rows_t, bounds, right=True).clamp_(max=nchunks - 1)
 
         nnz = lay.nnz
         idx = lay.idx[:nnz].long()
         row_of = lay.row_of[:nnz].long()
         cnt = torch.bincount(idx, minlength=n_gath)
-        order = torch.argsort(cnt, descending=True, stable=True)
-        rank = torch.empty_like(order)
-        rank[order] = torch.arange(n_gath, device=dev)
+        # panels: gathered rows by decreasing gather count -- inside their chunk
+        # when the gathered table is chunked -- PR rows per panel
+        allg = torch.arange(n_gath, device=dev)
+        gch = chunk_of(allg) if chunk_by == "gath" else torch.zeros(n_gath, dtype=torch.long, device=dev)
+        ngc = nchunks if chunk_by == "gath" else 1
+        cmax = int(cnt.max().item()) if n_gath else 0
+        order = torch.argsort(gch * (cmax + 1) + (cmax - cnt), stable=True)
+        gsize = torch.bincount(gch, minlength=ngc)
+        gstart0 = torch.cumsum(gsize, 0) - gsize
+        rank_in = torch.empty_like(order)
+        rank_in[order] = allg - gstart0[gch[order]]
         del cnt
-        npc = max(1, min((n_gath + PR - 1) // PR, max_panels))
-        pan_e = (rank // PR)[idx]
-        key = torch.where(pan_e < npc, pan_e, torch.full_like(pan_e, npc)).to(torch.int16)
+        sizes = gsize.cpu().tolist()
+        npc_c = [max(1, min((sz + PR - 1) // PR, max(1, int(round(max_panels * sz / max(n_gath, 1))))))
+                 if sz else 0 for sz in sizes]
+        pbase = [0]
+        for x in npc_c:
+            pbase.append(pbase[-1] + x)
+        npt = max(pbase[-1], 1)                       # panels over all chunks
+        pbase_t = torch.tensor(pbase[:-1], device=dev)
+        npc_t = torch.tensor(npc_c, device=dev)
+        pan_g = torch.where(rank_in < npc_t[gch] * PR, pbase_t[gch] + rank_in // PR,
+                            torch.full_like(rank_in, npt))
+        local_g = rank_in % PR
+        panel_chunk = torch.repeat_interleave(torch.arange(ngc, device=dev), npc_t) if pbase[-1] else \
+            torch.zeros(1, dtype=torch.long, device=dev)
+        pan_e = pan_g[idx]
+        key = pan_e.to(torch.int16)
         del pan_e
         skey, perm = torch.sort(key, stable=True)
         del key
-        nh = int((skey < npc).sum().item())
+        nh = int((skey < npt).sum().item())
         perm = perm[:nh]
         pkey = skey[:nh].long()
         del skey
@@ -117,21 +151,17 @@ class _PanelPass:
         plen = torch.diff(pstart, append=torch.tensor([nh], device=dev))
         ppanel = pkey[pstart]
         keep_piece = plen >= lmin
-        ent_panel = torch.zeros(npc, dtype=torch.long, device=dev)
+        ent_panel = torch.zeros(npt, dtype=torch.long, device=dev)
         ent_panel.index_add_(0, ppanel, plen * keep_piece)
-        ok = (ent_panel >= min_panel_entries).cpu()
-        npk = npc
-        for p in range(npc):
-            if not bool(ok[p]):
-                npk = p
-                break
-        keep_piece &= ppanel < npk
+        ok_p = ent_panel >= min_panel_entries       # panels worth loading
+        keep_piece &= ok_p[ppanel]
         piece_id = torch.cumsum(flag, 0) - 1
         keep_e = keep_piece[piece_id] if nh else flag
         del piece_id, flag
         hot_orig = perm[keep_e]                 # original positions, (panel, row, order)
         del perm, keep_e, pkey
-        self.n_panels = npk
+        npk = npt
+        self.n_panels = int(ok_p.sum().item())
         self.n_hot = int(hot_orig.numel())
         cold = torch.ones(nnz, dtype=torch.bool, device=dev)
         cold[hot_orig] = False
@@ -150,7 +180,7 @@ class _PanelPass:
         # panel's tail array (window = local row mod 4) where the piece allows:
         # the t-th entry of each window, for t = 0, 1, ...
         sub_of_e = torch.repeat_interleave(torch.arange(ns, device=dev), slen)
-        local = rank[idx[hot_orig]] % PR
+        local = local_g[idx[hot_orig]]
         if self.n_hot:
             key1 = sub_of_e * 4 + (local % 4)
             o1 = torch.argsort(key1, stable=True)
@@ -182,10 +212,10 @@ class _PanelPass:
         self.hot_pos = ppos
         # panel row ids
         ids = torch.full((max(npk, 1) * PR,), -1, dtype=torch.int32, device=dev)
-        nrows_hot = min(npk * PR, n_gath)
-        ids[:nrows_hot] = order[:nrows_hot].to(torch.int32)
+        hot_g = torch.nonzero(pan_g < npt).flatten()
+        ids[pan_g[hot_g] * PR + local_g[hot_g]] = hot_g.to(torch.int32)
         self.panel_ids = ids
-        del rank, order, local
+        del order, local, hot_g
         # cold pieces: a self row's cold entries in their order, cut at lmax;
         # record blocks of 16 x u32 gathered-row ids + 16 x f32 values
         nsc = 0
@@ -193,12 +223,26 @@ class _PanelPass:
             cold_orig = torch.nonzero(cold).flatten()
             ncold = int(cold_orig.numel())
             crow = row_of[cold_orig]
+            if chunk_by == "gath" and nchunks > 1:
+                # a cold piece gathers from one chunk: entries by (chunk of the
+                # gathered row, self row, original order)
+                cg = gch[idx[cold_orig]]
+                o_g = torch.argsort(cg, stable=True)
+                cold_orig, crow, cg = cold_orig[o_g], crow[o_g], cg[o_g]
+                ckey = cg * n_self + crow
+                del o_g
+            else:
+                cg = None
+                ckey = crow
             fc = torch.ones(ncold, dtype=torch.bool, device=dev)
             if ncold > 1:
-                fc[1:] = crow[1:] != crow[:-1]
+                fc[1:] = ckey[1:] != ckey[:-1]
             cps = torch.nonzero(fc).flatten()
             cpl = torch.diff(cps, append=torch.tensor([ncold], device=dev))
-            srow_c, span_c, slen_c, cstart_c = _cut(cpl, crow[cps], torch.full_like(cps, npk), lmax, dev)
+            pchunk = cg[cps] if cg is not None else None
+            del ckey
+            # (the panel slot of a cold sub-piece carries its gathered chunk when there is one)
+            srow_c, span_c, slen_c, cstart_c = _cut(cpl, crow[cps], pchunk if pchunk is not None else torch.full_like(cps, npk), lmax, dev)
             nsc = int(srow_c.numel())
             nblk_c = (slen_c + 15) // 16
             bstart_c = torch.cumsum(nblk_c, 0) - nblk_c
@@ -244,14 +288,15 @@ class _PanelPass:
         self.fbeg = fbeg[o_lh].to(torch.int32)
         self.fcnt = counts[o_lh].to(torch.int32)
         # piece table: per panel by decreasing length
-        span2 = span * nchunks + chunk_of(srow)             # (panel, chunk of the self row)
+        echunk = panel_chunk[span.clamp(max=panel_chunk.numel() - 1)] if chunk_by == "gath" else chunk_of(srow)
+        span2 = span * nchunks + echunk                     # (panel, chunk)
         o_pl = torch.argsort(span2 * (lmax + 1) + (lmax - slen), stable=True)
         pieces = torch.stack([srow[o_pl], bstart[o_pl], slen[o_pl], slot[:ns][o_pl]], dim=1).to(torch.int32)
         self.pieces = pieces.contiguous() if ns else torch.zeros((1, 4), dtype=torch.int32, device=dev)
         self.n_pieces = ns
         self.n_slots = nsa
         if cold_pieces:
-            chunk_c = chunk_of(srow_c)
+            chunk_c = span_c if pchunk is not None else chunk_of(srow_c)
             o_c = torch.argsort(chunk_c * (lmax + 1) + (lmax - slen_c), stable=True)
             cc_cnt = torch.bincount(chunk_c, minlength=nchunks).cpu().tolist() if nsc else [0] * nchunks
             self.cold_chunk_ptr = [0]
@@ -280,7 +325,7 @@ class _PanelPass:
             self.plist_entries = torch.zeros(0, dtype=torch.long)
             self.plist_chunk = torch.zeros(0, dtype=torch.long)
         # fold lists per chunk (light rows, then heavy rows, inside each chunk)
-        if nchunks > 1:
+        if nchunks > 1 and chunk_by == "self":
             fch = chunk_of(frows)
             o_cf = torch.argsort(fch * 2 + (counts > 32).long(), stable=True)
             self.cf_rows = frows[o_cf].to(torch.int32)
@@ -320,12 +365,13 @@ class _PanelPass:
         restricted to the chunk's self rows."""
         out = []
         for c in range(self.nchunks):
-            off, nr, nlt = self.cf_info[c]
             f = _lib.PanelPass.from_buffer_copy(self.c)
-            f.n_frows, f.n_light = nr, nlt
-            f.frows = self.cf_rows.data_ptr() + 4 * off
-            f.fbeg = self.cf_beg.data_ptr() + 4 * off
-            f.fcnt = self.cf_cnt.data_ptr() + 4 * off
+            if self.chunk_by == "self":
+                off, nr, nlt = self.cf_info[c]
+                f.n_frows, f.n_light = nr, nlt
+                f.frows = self.cf_rows.data_ptr() + 4 * off
+                f.fbeg = self.cf_beg.data_ptr() + 4 * off
+                f.fcnt = self.cf_cnt.data_ptr() + 4 * off
             g = _lib.PanelPass.from_buffer_copy(self.cc)
             c0, c1 = self.cold_chunk_ptr[c], self.cold_chunk_ptr[c + 1]
             g.n_pieces = c1 - c0
@@ -395,13 +441,16 @@ class HybridSweepPlan:
         lean = cold == "pieces"
         kw = dict(lmin=lmin, lmax=lmax, max_panels=max_panels, min_panel_entries=min_panel_entries,
                   cold_pieces=lean, direct=lean and self.ld == self.k)
-        self.p0 = _PanelPass(dev.csr, dev.vals, obs.m, obs.n, self.PR, self.ld, 0, want_r=False,
-                             want_sq=True, **kw)
-        # the CSC pass in column chunks: the end-to-end path moves H, computes and
-        # returns R^T.W chunk by chunk (cold="pieces" plans)
+        # H in column chunks (cold="pieces" plans): the end-to-end path moves H, runs
+        # the work that needs a chunk and returns R^T.W chunk by chunk. The CSC pass
+        # is cut by its self rows, the CSR pass by the rows it gathers.
         self.nchunks = int(env("MFG_PANEL_CHUNKS", 4)) if lean else 1
+        crows = _chunk_rows(obs.n, self.nchunks, float(env("MFG_PANEL_CHUNK_RATIO", 0.7)))
+        self.nchunks = len(crows) - 1
+        self.p0 = _PanelPass(dev.csr, dev.vals, obs.m, obs.n, self.PR, self.ld, 0, want_r=False,
+                             want_sq=True, chunk_rows=crows, chunk_by="gath", **kw)
         self.p1 = _PanelPass(dev.csc, dev.vals_csc, obs.n, obs.m, self.PR, self.ld, 1,
-                             want_r=False, want_sq=False, nchunks=self.nchunks, **kw)
+                             want_r=False, want_sq=False, chunk_rows=crows, chunk_by="self", **kw)
         # one list over both passes; the CSC pass's piece indices are its own
         self.plist = torch.cat([self.p0.plist, self.p1.plist], 0).contiguous()
         self.n_list = int(self.plist.shape[0])
@@ -430,13 +479,18 @@ class HybridSweepPlan:
             self._pass_lists.append((nl, pp.plist.contiguous(), cs,
                                      torch.zeros(nl + 2, dtype=torch.int32, device=dev.device)))
         self._chunk_lists = []
-        if self.p1.nchunks > 1:
-            for c in range(self.p1.nchunks):
-                sel = torch.nonzero(self.p1.plist_chunk == c).flatten()
-                nl = int(sel.numel())
+        if lean and self.nchunks > 1:
+            for c in range(self.nchunks):
+                parts, ents = [], []
+                for pp in (self.p0, self.p1):
+                    sel = torch.nonzero(pp.plist_chunk == c).flatten()
+                    if sel.numel():
+                        parts.append(pp.plist[sel.to(dev.device)])
+                        ents.append(pp.plist_entries[sel].double())
+                nl = int(sum(x.shape[0] for x in parts))
                 if nl:
-                    pl = self.p1.plist[sel.to(dev.device)].contiguous()
-                    ed = torch.cumsum(self.p1.plist_entries[sel].double(), 0)
+                    pl = torch.cat(parts, 0).contiguous()
+                    ed = torch.cumsum(torch.cat(ents), 0)
                     at = (torch.arange(nctas, dtype=torch.float64) + 0.5) * float(ed[-1]) / nctas
                     cs = torch.searchsorted(ed, at).clamp_(max=nl - 1).to(torch.int32).to(dev.device)
                 else:
@@ -444,7 +498,6 @@ class HybridSweepPlan:
                     cs = torch.zeros(nctas, dtype=torch.int32, device=dev.device)
                 self._chunk_lists.append((nl, pl, cs, torch.zeros(nl + 2, dtype=torch.int32,
                                                                   device=dev.device)))
-            self._chunk_structs = self.p1.chunk_structs()
         nnz = obs.size
         self.want_r = want_r
         nh_pad = (self.p0.n_blocks + 2) * 16
@@ -505,6 +558,9 @@ class HybridSweepPlan:
         self._ev_w = torch.cuda.Event()
         self._ev_h = [torch.cuda.Event() for _ in range(max(self.nchunks, 1))]
         self._ev_f = [torch.cuda.Event() for _ in range(max(self.nchunks, 1))]
+        if self._chunk_lists:
+            self._chunk_structs0 = self.p0.chunk_structs()
+            self._chunk_structs1 = self.p1.chunk_structs()
         self.stats = {
             "panel_rows": self.PR, "csr_panels": self.p0.n_panels, "csc_panels": self.p1.n_panels,
             "csr_hot": self.p0.n_hot, "csc_hot": self.p1.n_hot, "nnz": nnz,
@@ -610,16 +666,19 @@ class HybridSweepPlan:
             cur.wait_event(self._ev_join)
 
     def _host_call_chunked(self, w_host, h_host):
-        """The end-to-end step as a pipeline over column chunks: H moves to the
-        device chunk by chunk on a copy-in stream; as soon as a chunk of H has
-        arrived the CSC pass runs on its columns (cold pieces, panel pieces,
-        fold) and the chunk's rows of R^T.W return on a copy-out stream; the
-        CSR pass (which gathers all of H) follows the last chunk."""
+        """The end-to-end step as a pipeline over chunks of H (contiguous row
+        ranges): W, then H chunk by chunk, move to the device on a copy-in
+        stream. As soon as chunk c has arrived, the work that needs it runs: the
+        CSC pass on the chunk's columns (their rows of R^T.W are folded and
+        return on a copy-out stream) and the CSR pass's pieces that gather from
+        the chunk (panels hold rows of one chunk; cold pieces gather from one
+        chunk). The CSR fold, sum r^2, the norms, the R gather and
+        [sums | R.H] follow the last chunk."""
         lib = _lib.lib()
         m, n, k, ld = self.obs.m, self.obs.n, self.k, self.ld
         cur = torch.cuda.current_stream()
         cin, cout = self._cin, self._copy
-        nc = self.p1.nchunks
+        nc = self.nchunks
         cr = self.p1.chunk_rows
         self._ev_start.record(cur)
         cin.wait_event(self._ev_start)
@@ -632,21 +691,24 @@ class HybridSweepPlan:
                 self._ev_h[c].record(cin)
         cur.wait_event(self._ev_w)
         st = cur.cuda_stream
-        none = ctypes.byref(self._no_cold)
         nb_head = 32 + self.RH.numel() * 4
+        self.sums[0:1].zero_()
+        _lib.check(lib.mfg_dot(_lib.MFG_F32, m * ld, self._wd.data_ptr(), self._wd.data_ptr(),
+                               self.sums.data_ptr() + 8, self.ws.data_ptr(), self.wsb, st), "norm")
         for c in range(nc):
             cur.wait_event(self._ev_h[c])
-            fold_c, cold_c = self._chunk_structs[c]
-            _lib.check(lib.mfg_cold_sweep(ld, none, ctypes.byref(cold_c), self._wd.data_ptr(),
-                                          self._hd.data_ptr(), self.RH.data_ptr(), self.RtW.data_ptr(),
-                                          self.out_scale, self.cold_counters.data_ptr(), st),
-                       "cold sweep")
+            cold0 = self._chunk_structs0[c][1]
+            fold1, cold1 = self._chunk_structs1[c]
+            _lib.check(lib.mfg_cold_sweep(ld, ctypes.byref(cold0), ctypes.byref(cold1),
+                                          self._wd.data_ptr(), self._hd.data_ptr(), self.RH.data_ptr(),
+                                          self.RtW.data_ptr(), self.out_scale,
+                                          self.cold_counters.data_ptr(), st), "cold sweep")
             nl, plist, cs, cnt = self._chunk_lists[c]
             if nl:
                 _lib.check(lib.mfg_panel_sweep(ld, nl, plist.data_ptr(), cs.data_ptr(), self.p0.ref,
                                                self.p1.ref, self._wd.data_ptr(), self._hd.data_ptr(),
                                                cnt.data_ptr(), st), "panel sweep")
-            _lib.check(lib.mfg_panel_fold(ld, k, ctypes.byref(fold_c), self.RtW.data_ptr(), k,
+            _lib.check(lib.mfg_panel_fold(ld, k, ctypes.byref(fold1), self.RtW.data_ptr(), k,
                                           self.out_scale, 1, None, None, st), "panel fold")
             self._ev_f[c].record(cur)
             cout.wait_event(self._ev_f[c])
@@ -654,7 +716,20 @@ class HybridSweepPlan:
             with torch.cuda.stream(cout):
                 self._host[b0:b1].copy_(self._out[b0:b1], non_blocking=True)
         self._ev_copy.record(cout)
-        pending = self._enqueue_pass(self._wd, self._hd, 0)
+        # all of H is here: its norm, the CSR pass's fold and sum r^2, R in CSR order
+        _lib.check(lib.mfg_dot(_lib.MFG_F32, n * ld, self._hd.data_ptr(), self._hd.data_ptr(),
+                               self.sums.data_ptr() + 16, self.ws.data_ptr(), self.wsb, st), "norm")
+        pending = False
+        if self.want_r:
+            self._ev_fork.record(cur)
+            self._side.wait_event(self._ev_fork)
+            _lib.check(lib.mfg_gather(_lib.MFG_F32, self.obs.size, self._rsrc.data_ptr(),
+                                      self._rcat.data_ptr(), self.R.data_ptr(), self._side.cuda_stream),
+                       "R gather")
+            self._ev_join.record(self._side)
+            pending = True
+        _lib.check(lib.mfg_panel_fold(ld, k, self.p0.ref, self.RH.data_ptr(), k, self.out_scale, 1,
+                                      self.sums.data_ptr(), self.sq_ws.data_ptr(), st), "panel fold")
         self._host[:nb_head].copy_(self._out[:nb_head], non_blocking=True)
         if pending:
             cur.wait_event(self._ev_join)

@@ -166,11 +166,12 @@ def test_panel_layout_chunks():
     lay = types.SimpleNamespace(nnz=len(rows), nrows=m, ncols=n, idx=torch.tensor(cols, dtype=torch.int32),
                                 row_of=torch.tensor(rows, dtype=torch.int32))
     nc = 3
+    crows = panel._chunk_rows(m, nc, 0.7)
     pp = panel._PanelPass(lay, torch.tensor(vals), m, n, 16, k, 1, lmin=3, lmax=21, max_panels=6,
                           min_panel_entries=10, want_r=False, want_sq=False, cold_pieces=True,
-                          direct=True, nchunks=nc)
+                          direct=True, chunk_rows=crows, chunk_by="self")
     cr = pp.chunk_rows
-    assert cr[0] == 0 and cr[-1] == m and len(cr) == nc + 1
+    assert cr[0] == 0 and cr[-1] == m and len(cr) == nc + 1 and cr[1] - cr[0] > cr[3] - cr[2]
     pieces = pp.pieces.numpy()
     panels = []
     for (_, p, a, b), c in zip(pp.plist.numpy(), pp.plist_chunk.numpy()):
@@ -194,3 +195,65 @@ def test_panel_layout_chunks():
         tot += nr
     assert tot == pp.frows.numel()
     assert sorted(pp.cf_rows.numpy().tolist()) == sorted(pp.frows.numpy().tolist())
+
+
+def test_panel_layout_gathered_chunks():
+    """chunk_by="gath" (the end-to-end path's CSR pass): a panel holds gathered
+    rows of one chunk, a cold piece gathers from one chunk, and the replay
+    still reproduces R.H."""
+    m, n, k = 60, 300, 40
+    rng, rows, cols, vals = _case(4, m, n, 0.5, 0.4)
+    nnz = len(rows)
+    lay = types.SimpleNamespace(nnz=nnz, nrows=m, ncols=n, idx=torch.tensor(cols, dtype=torch.int32),
+                                row_of=torch.tensor(rows, dtype=torch.int32))
+    nc, PR = 3, 16
+    crows = panel._chunk_rows(n, nc, 0.7)
+    pp = panel._PanelPass(lay, torch.tensor(vals), m, n, PR, k, 0, lmin=3, lmax=21, max_panels=9,
+                          min_panel_entries=10, want_r=False, want_sq=True, cold_pieces=True,
+                          direct=True, chunk_rows=crows, chunk_by="gath")
+    assert pp.n_hot > 0 and pp.n_cold_pieces > 0
+    W = rng.standard_normal((m, k))
+    H = rng.standard_normal((n, k))
+    ids = pp.panel_ids.numpy()
+    recs = pp.recs.numpy()
+    loc16 = recs.view(np.int16).reshape(-1, 48)
+    po = np.zeros((pp.n_slots, k))
+    RH = np.zeros((m, k))
+    pieces = pp.pieces.numpy()
+    for (_, p, a, b), c in zip(pp.plist.numpy(), pp.plist_chunk.numpy()):
+        prow = ids[p * PR:(p + 1) * PR]
+        live = prow[prow >= 0]
+        assert np.all((live >= crows[c]) & (live < crows[c + 1]))    # the panel's rows: one chunk
+        for row, blk0, ln, slot in pieces[a:b]:
+            for e in range(ln):
+                blk, off = blk0 + e // 16, e % 16
+                g = prow[loc16[blk, off]]
+                assert g >= 0
+                a_e = float(recs[blk, 8 + off:9 + off].view(np.float32)[0])
+                po[slot] += (float(W[row] @ H[g]) - a_e) * H[g]
+    crecs = pp.cold_recs.numpy()
+    cp = pp.cold_pieces.numpy()
+    ptr = pp.cold_chunk_ptr
+    assert ptr[-1] == pp.n_cold_pieces
+    for c in range(nc):
+        for row, blk0, ln, slot in cp[ptr[c]:ptr[c + 1]]:
+            is_direct = (ln >> 30) != 0
+            ln &= 0x3fffffff
+            for e in range(ln):
+                blk, off = blk0 + e // 16, e % 16
+                g = crecs[blk, off]
+                assert crows[c] <= g < crows[c + 1]                    # gathers from its chunk only
+                a_e = float(crecs[blk, 16 + off:17 + off].view(np.float32)[0])
+                r = float(W[row] @ H[g]) - a_e
+                if is_direct:
+                    RH[row] += r * H[g]
+                else:
+                    po[slot] += r * H[g]
+    fr, fb, fc = pp.frows.numpy(), pp.fbeg.numpy(), pp.fcnt.numpy()
+    for f, row in enumerate(fr):
+        RH[row] += po[fb[f]:fb[f] + fc[f]].sum(0)
+    Rfull = (W[rows] * H[cols]).sum(1) - vals.astype(np.float64)
+    RHref = np.zeros((m, k))
+    np.add.at(RHref, rows, Rfull[:, None] * H[cols])
+    assert np.abs(RH - RHref).max() < 1e-11
+    assert len(pp.cold_orig) + pp.n_hot == nnz
