@@ -445,7 +445,19 @@ class HybridSweepPlan:
         # the work that needs a chunk and returns R^T.W chunk by chunk. The CSC pass
         # is cut by its self rows, the CSR pass by the rows it gathers.
         self.nchunks = int(env("MFG_PANEL_CHUNKS", 4)) if lean else 1
-        crows = _chunk_rows(obs.n, self.nchunks, float(env("MFG_PANEL_CHUNK_RATIO", 0.7)))
+        # relative chunk sizes: a small first chunk (the first work starts early), a
+        # small last one (its R^T.W rows return after the last fold); the kernels,
+        # not the transfers, bound the step, so the chunks in between are large
+        sizes = env("MFG_PANEL_CHUNK_SIZES", "5,15,25,25,20,10" if "MFG_PANEL_CHUNKS" not in os.environ else "")
+        if sizes and lean:
+            wts = [float(x) for x in sizes.split(",")]
+            acc, crows = 0.0, [0]
+            for i, x in enumerate(wts):
+                acc += x
+                crows.append(obs.n if i == len(wts) - 1 else
+                             max(crows[-1], min(obs.n, int(round(obs.n * acc / sum(wts))))))
+        else:
+            crows = _chunk_rows(obs.n, self.nchunks, float(env("MFG_PANEL_CHUNK_RATIO", 0.7)))
         self.nchunks = len(crows) - 1
         self.p0 = _PanelPass(dev.csr, dev.vals, obs.m, obs.n, self.PR, self.ld, 0, want_r=False,
                              want_sq=True, chunk_rows=crows, chunk_by="gath", **kw)
@@ -556,8 +568,8 @@ class HybridSweepPlan:
         self._cin = torch.cuda.Stream(device=dev.device)
         self._ev_start = torch.cuda.Event()
         self._ev_w = torch.cuda.Event()
-        self._ev_h = [torch.cuda.Event() for _ in range(max(self.nchunks, 1))]
-        self._ev_f = [torch.cuda.Event() for _ in range(max(self.nchunks, 1))]
+        self._ev_h = [torch.cuda.Event() for _ in range(max(self.nchunks, 1) + 16)]
+        self._ev_f = [torch.cuda.Event() for _ in range(max(self.nchunks, 1) + 16)]
         if self._chunk_lists:
             self._chunk_structs0 = self.p0.chunk_structs()
             self._chunk_structs1 = self.p1.chunk_structs()
