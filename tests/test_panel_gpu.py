@@ -167,3 +167,36 @@ def test_hybrid_out_scale_and_no_r(cold):
     assert np.max(np.abs(_np(plan.RH) - 2.0 * rh3)) <= 4e-4 * sc(rh3)
     assert np.max(np.abs(_np(plan.RtW) - 2.0 * rtw3)) <= 4e-4 * sc(rtw3)
     assert plan.sums.cpu().numpy()[0] == pytest.approx(sq3, rel=2e-4)
+
+
+@pytest.mark.parametrize("k", [40, 30])
+@pytest.mark.parametrize("sizes", ["5,15,25,25,20,10", "100", "50,50", "1,1,1,1,1,1,1,1,1,1,1,1"])
+def test_hybrid_run_host_chunk_profiles(k, sizes, monkeypatch):
+    """The end-to-end pipeline over chunks of H (any chunk profile, padded and
+    unpadded factor rows) is bitwise equal to the resident sweep, eagerly and as
+    a replayed CUDA graph, and matches the oracle."""
+    from paper_2204_14067_b200.panel import HybridSweepPlan
+    monkeypatch.setenv("MFG_PANEL_CHUNK_SIZES", sizes)
+    m, n, r, c, v = synth.generate("c3", scale=0.03, seed=300 + k)
+    m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
+    v32 = v.astype(np.float32).astype(np.float64)
+    om = orc.from_coo(m, n, r, c, v32)
+    obs = D.ObservationSet.from_coo(m, n, r, c, v32, dtype=torch.float32)
+    w, h = synth.sweep_factors(m, n, k, seed=6)
+    plan = HybridSweepPlan(obs, k)
+    assert plan.nchunks == len(sizes.split(","))
+    wt = torch.as_tensor(w).float().cuda()
+    ht = torch.as_tensor(h).float().cuda()
+    _check(plan, om, wt, ht, k)
+    ref = [plan.sums.clone().cpu(), plan.RH.clone().cpu(), plan.RtW.clone().cpu()]
+    R0 = plan.R.clone()
+    wa, ha = plan.pinned_factors()
+    wa.copy_(torch.as_tensor(w).float())
+    ha.copy_(torch.as_tensor(h).float())
+    for graph in (False, True, True):
+        plan.R.zero_()
+        out = plan.run_host(wa, ha, graph=graph)
+        torch.cuda.synchronize()
+        for x, y in zip(out, ref):
+            assert torch.equal(x, y)
+        assert torch.equal(plan.R, R0)
