@@ -11,6 +11,9 @@ run a full c4 sweep in test time:
   fp32 accumulation, ``_fp32_sum_bound``);
 * Omega index handling: CSR rows sorted, CSC order = stable argsort of the
   columns (bit-exact), and bitwise run-to-run determinism of the sweep.
+
+Both sweep plans are checked: the gather sweep at c3-c5 and the hybrid panel
+sweep (the plan bench.py runs at c4) at c3 and c4.
 """
 
 import os
@@ -30,18 +33,24 @@ def _fp32_sum_bound(terms, ref_row) -> float:
     return float((1e-5 * terms.abs().sum(0) + 2e-5 * ref_row.abs()).max()) + 1e-6
 
 
-@pytest.mark.parametrize("wl", WORKLOADS)
-def test_full_size_sweep_properties(wl):
+@pytest.mark.parametrize("wl,kind", [(w, "gather") for w in WORKLOADS] + [("c3", "hybrid"), ("c4", "hybrid")])
+def test_full_size_sweep_properties(wl, kind):
+    """kind = "gather": the grouped gather sweep (mfsolver.SweepPlan); "hybrid":
+    the panel sweep (panel.HybridSweepPlan: k_panel4 + k_cold4), the plan the
+    bench runs at c4."""
     from paper_2204_14067_b200 import synth
     from paper_2204_14067_b200.data import ObservationSet
     from paper_2204_14067_b200.mfsolver import SweepPlan
+    from paper_2204_14067_b200.panel import HybridSweepPlan
 
     m, n, r, c, v = synth.generate(wl, seed=0)
     m, n, r, c, v, _ = synth.canonical(m, n, r, c, v)
     k = synth.CONFIGS[wl].k0
     obs = ObservationSet.from_coo(m, n, r, c, v, dtype=torch.float32)
     w_np, h_np = synth.sweep_factors(m, n, k, seed=5, dtype=np.float32)
-    plan = SweepPlan(obs, k, compute_f64=False)
+    plan = SweepPlan(obs, k, compute_f64=False) if kind == "gather" else HybridSweepPlan(obs, k)
+    if kind == "hybrid":
+        assert plan.stats["csr_hot"] > obs.size // 2 and plan.stats["csc_hot"] > obs.size // 2
     w = plan.pad(torch.as_tensor(w_np, device="cuda"))
     h = plan.pad(torch.as_tensor(h_np, device="cuda"))
     plan.run(w, h)
