@@ -15,6 +15,7 @@ from . import _lib
 from .data import ObservationSet
 from .kernels import SIGMA_FLOOR, SvdTriplet, as_device
 from .operators import FactorPair
+from ._nvtx import annotate
 
 _GUARD_SLACK = 1e-9          # mfg/mfsolver.py:15
 _GUARD_SLACK_F32 = 1e-6      # fp32 storage: rounding of the stored factors
@@ -226,6 +227,7 @@ def sweep(obs: ObservationSet, wf: FactorPair, *, want_r=False, want_rh=False, w
     return plan.R, plan.RH, plan.RtW, plan.sums.cpu().numpy()
 
 
+@annotate("mfg.mf_objective")
 def mf_objective(obs: ObservationSet, wf: FactorPair, lam: float) -> float:
     """f(W H^T) + (lam/2)(||W||^2 + ||H||^2) (mfg/mfsolver.py:48-50)."""
     if wf.w.shape[0] != obs.m or wf.h.shape[0] != obs.n:
@@ -237,6 +239,7 @@ def mf_objective(obs: ObservationSet, wf: FactorPair, lam: float) -> float:
     return float(s[0]) + 0.5 * lam * (float(s[1]) + float(s[2]))
 
 
+@annotate("mfg._half_sweep")
 def _half_sweep(obs: ObservationSet, transpose: bool, other: torch.Tensor, lam: float) -> torch.Tensor:
     dev = obs.dev
     lay = dev.csc if transpose else dev.csr
@@ -279,6 +282,7 @@ def check_bcd_status(sync: bool = True) -> None:
         raise NumericalError("BCD half-sweep: non-SPD normal matrix (non-finite factors or data)")
 
 
+@annotate("mfg.bcd_epoch")
 def bcd_epoch(obs: ObservationSet, wf: FactorPair, lam: float) -> FactorPair:
     """All rows of W given H, then all rows of H given the new W (78-93)."""
     if lam <= 0:
@@ -293,6 +297,7 @@ def bcd_epoch(obs: ObservationSet, wf: FactorPair, lam: float) -> FactorPair:
     return FactorPair(w_new, h_new)
 
 
+@annotate("mfg.mf_phase")
 def mf_phase(obs: ObservationSet, start: FactorPair, lam: float, epochs: int) -> FactorPair:
     """``epochs`` BCD sweeps with the monotone-descent guard (96-112)."""
     wf = start
