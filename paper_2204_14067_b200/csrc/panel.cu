@@ -1,42 +1,49 @@
-// Panel passes of the Omega sweep: the hot part of a pass with the gathered
-// factor rows staged in shared memory.
+// The piece sweep: every entry of a pass belongs to a *piece* -- a run of one
+// self row's entries -- and 4- or 8-lane groups walk pieces; the gathered
+// factor rows of the hot pieces come from shared-memory panels.
 //
 // The sweep's two passes (CSR: r = w_i.h_j - a, R.H; CSC: the same residual,
 // R^T.W; mfg/data.py:253-263, mfg/operators.py:108,117) gather one k-wide
 // factor row per entry. With every gather served by L2 the sweep is bound by
 // the L2->SM crossbar (K4). Gather counts are Zipf-skewed, so most
 // gathers go to a few thousand rows: this file runs those entries from
-// *panels* -- sets of PR gathered rows held in one SM's shared memory (208 KB)
-// -- and leaves the remaining (cold) entries to the gather kernel in sweep.cu.
+// *panels* -- sets of PR gathered rows held in one SM's shared memory (200 KB)
+// -- with k_panel4 (rows of one 32-dim block, k <= 40) or k_panel (k = 64),
+// and the remaining (cold) entries as pieces on global loads with k_cold4 (or,
+// for k = 64, through the gather kernel in sweep.cu).
 //
 // Layout (built once per Omega and k by panel.py):
 //   panel_ids [NP][PR]   global gathered-row id of each panel slot (-1: none)
 //   pieces    [NPC]      {self row, first record block, length, output slot}:
-//                        a run of entries of one self row inside one panel, at
-//                        most Lmax entries; listed per panel by decreasing length
-//   recs                 record blocks of 16 entries (96 B): 16 x u16 panel-local
-//                        rows, then 16 x f32 A values. A piece owns whole blocks
-//                        (zero padded). Inside a piece the entries are ordered so
-//                        that the 4 entries of a batch fall into different
-//                        32-byte bank windows of the tail array where possible.
-//   plist     [NL]       {pass, panel, first piece, end piece}, one per panel
+//                        a run of entries of one self row inside one panel (hot)
+//                        or of its cold entries, at most Lmax entries; listed by
+//                        decreasing length (hot pieces: per panel and chunk)
+//   recs                 hot: record blocks of 16 entries (96 B): 16 x u16 panel-
+//                        local rows, then 16 x f32 A values; cold: 128 B blocks of
+//                        16 x u32 gathered-row ids, 16 x f32 A. A piece owns whole
+//                        blocks (zero padded). Inside a hot piece the entries are
+//                        ordered so that the 4 entries of a batch fall into
+//                        different 32-byte bank windows of the tail array where
+//                        possible.
+//   plist     [NL]       {pass, panel, first piece, end piece}, panel-major
 //   cta_start [CTAs]     the list element each CTA starts at (work-proportional)
-//   frows / fbeg / fcnt  self rows that own pieces and their slot ranges;
-//                        slots are numbered in (self row, panel, run) order
+//   frows / fbeg / fcnt  self rows that own slots and their slot ranges; slots are
+//                        numbered in (self row, panel, run) order, cold pieces last
 //
-// k_panel: persistent CTAs (one per SM) walk the panel list cyclically from
-// their start element; a CTA loads a panel that still has pieces with cp.async,
-// then its warps take rounds of 4 pieces (one per 8-lane group) from the
-// panel's global ticket, the next round's descriptors and self rows loading
-// during the current one. Records stream through a per-group cp.async ring.
-// Per 4 entries a group issues 4 conflict-free LDS.128 of the rows' first 128
-// bytes (lane q holds dims [4q, 4q+4) of 32-dim blocks), one LDS.128 of the 4
-// entries' tail chunks (k = 40: dims 32..39, lane q holds chunk q&1 of entry
-// q>>1), a transposed 8-lane butterfly that leaves entry q>>1's dot in lanes
-// 2(q>>1), 2(q>>1)+1, and the accumulation of r * row in registers. A piece
-// writes its partial output vector to its slot; k_panel_fold adds a self row's
-// slots in slot order to the cold part, so the result does not depend on which
-// CTA ran which piece (bitwise reproducible).
+// k_panel (8-lane groups; k_panel4 below is the 4-lane version): persistent
+// CTAs (one per SM) walk the panel list cyclically from their start element; a
+// CTA loads a panel that still has pieces with cp.async, then its warps take
+// rounds of 4 pieces (one per 8-lane group) from the element's global ticket,
+// the next round's descriptors and self rows loading during the current one.
+// Records stream through a per-group cp.async ring. Per 4 entries a group
+// issues 4 conflict-free LDS.128 of the rows' first 128 bytes (lane q holds
+// dims [4q, 4q+4) of 32-dim blocks), one LDS.128 of the 4 entries' tail chunks
+// (k = 40: dims 32..39, lane q holds chunk q&1 of entry q>>1), a transposed
+// 8-lane butterfly that leaves entry q>>1's dot in lanes 2(q>>1), 2(q>>1)+1,
+// and the accumulation of r * row in registers. A piece writes its partial
+// output vector to its slot; k_panel_fold sums a self row's slots in slot
+// order, so the result does not depend on which CTA ran which piece (bitwise
+// reproducible for a given layout).
 #include <stdlib.h>
 
 #include "common.cuh"
