@@ -295,6 +295,20 @@ int mfg_gemm_nn(int m, int p, int q, const double* A, int lda, const double* B,
                 int ldb, double alpha, double beta, double* C, int ldc,
                 void* stream);
 
+/* ---- tall-skinny QR of the lifting step --------------------------------
+ * Q (m x p, orthonormal columns) and diag[j] = |R_jj| of B = Q R for a
+ * row-major B (m x p, m >= p >= 1): the Householder QR of orthonormalize
+ * (mfg/kernels.py:76-105, np.linalg.qr + the |R_jj| <= tol ||B||_F column
+ * screening, which the caller applies to diag on the host) and of
+ * svd_from_factors (mfg/mfsolver.py:35-45). 32-column panels: block
+ * Gram-Schmidt with re-orthogonalisation against the finished columns (on
+ * the DMMA products above) around a Householder TSQR of the panel in shared
+ * memory. Q equals LAPACK's up to column signs. The workspace's first bytes
+ * are a mfg_gemm_tn workspace (zero before the first use, left zero).     */
+size_t mfg_qr_workspace(int m, int p);
+int mfg_qr(int m, int p, const double* B, int ldb, double* Q, int ldq,
+           double* diag, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- dense reductions ---------------------------------------------------
  * sums_host-free fp64 dot: out[0] = sum_i x_i y_i over `count` entries.    */
 int mfg_dot(int dtype, int64_t count, const void* x, const void* y,

@@ -109,6 +109,8 @@ _SIGS = {
     "mfg_bcd_status": (_INT, [_P, _P, _P]),
     "mfg_gemm_tn_workspace": (_SZ, [_INT, _INT, _INT]),
     "mfg_gemm_tn": (_INT, [_INT, _INT, _INT, _P, _INT, _P, _INT, _D, _P, _INT, _P, _SZ, _P]),
+    "mfg_qr_workspace": (_SZ, [_INT, _INT]),
+    "mfg_qr": (_INT, [_INT, _INT, _P, _INT, _P, _INT, _P, _P, _SZ, _P]),
     "mfg_gemm_nn": (_INT, [_INT, _INT, _INT, _P, _INT, _P, _INT, _D, _D, _P, _INT, _P]),
     "mfg_dot": (_INT, [_INT, _I64, _P, _P, _P, _P, _SZ, _P]),
     "mfg_profile_enable": (_INT, [_INT]),

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmfg_b200.so")
 OBJDIR = os.path.join(HERE, "build")
-SOURCES = ["abi.cu", "omega_build.cu", "sweep.cu", "panel.cu", "spmm.cu", "bcd.cu", "dense.cu", "ingest.cpp"]
+SOURCES = ["abi.cu", "omega_build.cu", "sweep.cu", "panel.cu", "spmm.cu", "bcd.cu", "dense.cu", "qr.cu", "ingest.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [*os.environ.get("MFG_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]

@@ -255,6 +255,13 @@ extern "C" int mfg_gemm_nn(int m, int p, int q, const double* A, int lda, const 
   return gemm_nn(m, p, q, A, lda, B, ldb, alpha, beta, C, ldc, (cudaStream_t)stream);
 }
 
+extern "C" size_t mfg_qr_workspace(int m, int p) { return qr_workspace(m, p); }
+
+extern "C" int mfg_qr(int m, int p, const double* B, int ldb, double* Q, int ldq, double* diag,
+                      void* workspace, size_t ws_bytes, void* stream) {
+  return qr_factor(m, p, B, ldb, Q, ldq, diag, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
 extern "C" int mfg_bcd_status(const void* workspace, int* flag_host, void* stream) {
   MFG_REQUIRE(workspace && flag_host, "null workspace or flag");
   // the half-sweep's non-SPD flag is the workspace's first word (bcd.cu do_bcd)

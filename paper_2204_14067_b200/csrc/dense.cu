@@ -131,11 +131,11 @@ __global__ void __launch_bounds__(128) k_gemm_tn(int m, int p, int q, const doub
   if (tid == 0) cnt[tile] = 0u;   // at rest for the next call
 }
 
-// C (m x q) = alpha * A (m x p) B (p x q) + beta * C
+// C (m x q) = alpha * A (m x p) B (p x q) + beta * Cin (Cin may be C itself)
 __global__ void __launch_bounds__(128) k_gemm_nn(int m, int p, int q, const double* __restrict__ A,
                                                  int lda, const double* __restrict__ B, int ldb,
-                                                 double alpha, double beta, double* __restrict__ C,
-                                                 int ldc) {
+                                                 double alpha, double beta, double* C, int ldc,
+                                                 const double* Cin, int ldcin) {
   __shared__ __align__(16) double sA[kT][kLdN];
   __shared__ __align__(16) double sB[kKC][kLdW];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(128) k_gemm_nn(int m, int p, int q, const doub
         if (r < m && c < q) {
           double* o = C + (int64_t)r * ldc + c;
           const double v = alpha * acc[i][j][h];
-          *o = beta == 0.0 ? v : fma(beta, *o, v);
+          *o = beta == 0.0 ? v : fma(beta, Cin[(int64_t)r * ldcin + c], v);
         }
       }
 }
@@ -248,7 +248,11 @@ int gemm_tn(int m, int p, int q, const double* A, int lda, const double* B, int 
 }
 
 int gemm_nn(int m, int p, int q, const double* A, int lda, const double* B, int ldb, double alpha,
-            double beta, double* C, int ldc, cudaStream_t stream) {
+            double beta, double* C, int ldc, cudaStream_t stream, const double* Cin, int ldcin) {
+  if (!Cin) {
+    Cin = C;
+    ldcin = ldc;
+  }
   MFG_REQUIRE(m >= 0 && p >= 0 && q >= 0, "negative size");
   MFG_REQUIRE(lda >= p && ldb >= q && ldc >= q, "leading dimension too small");
   if (m == 0 || q == 0) return MFG_OK;
@@ -257,7 +261,7 @@ int gemm_nn(int m, int p, int q, const double* A, int lda, const double* B, int 
     return MFG_OK;
   }
   dim3 grid((m + kT - 1) / kT, (q + kT - 1) / kT);
-  k_gemm_nn<<<grid, 128, 0, stream>>>(m, p, q, A, lda, B, ldb, alpha, beta, C, ldc);
+  k_gemm_nn<<<grid, 128, 0, stream>>>(m, p, q, A, lda, B, ldb, alpha, beta, C, ldc, Cin, ldcin);
   MFG_LAUNCH_CHECK();
   return MFG_OK;
 }

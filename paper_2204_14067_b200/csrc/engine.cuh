@@ -20,7 +20,11 @@ size_t gemm_tn_workspace(int m, int p, int q);
 int gemm_tn(int m, int p, int q, const double* A, int lda, const double* B, int ldb, double alpha,
             double* C, int ldc, void* ws, size_t wsb, cudaStream_t stream);
 int gemm_nn(int m, int p, int q, const double* A, int lda, const double* B, int ldb, double alpha,
-            double beta, double* C, int ldc, cudaStream_t stream);
+            double beta, double* C, int ldc, cudaStream_t stream, const double* Cin = nullptr,
+            int ldcin = 0);
+size_t qr_workspace(int m, int p);
+int qr_factor(int m, int p, const double* B, int ldb, double* Q, int ldq, double* diag, void* ws,
+              size_t wsb, cudaStream_t stream);
 int sddmm_dispatch(int dtype, int compute_f64, const mfg_layout* lay, int k, const void* L,
                    int ldl, const double* scale, const void* Rt, int ldr, const void* A,
                    const void* G, double out_mult, void* out, double* sums, void* ws, size_t wsb,

@@ -9,6 +9,10 @@ mfg/proxlift.py:127-314).
 * ``matmul(a, b)``    a b     (tall a times a small b), optional
                       ``alpha``, ``beta`` and ``out``
 * ``project_out(q, x)``  x - q (q^T x)
+* ``qr(b)``           (Q, |diag R|) of the tall-skinny QR b = Q R (csrc/qr.cu:
+                      block Gram-Schmidt with re-orthogonalisation around a
+                      Householder TSQR of 32-column panels), replacing
+                      LAPACK/cuSOLVER geqrf + orgqr (mfg/kernels.py:94)
 
 Inputs are fp64 device tensors (made contiguous, 1-d vectors as columns);
 results are bitwise reproducible run to run."""
@@ -94,3 +98,24 @@ def project_out(q: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
     out = xm.clone()
     matmul(q, gram(q, xm), alpha=-1.0, beta=1.0, out=out)
     return out[:, 0] if vec else out
+
+
+def qr(b: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """(Q, d): Q (m x p) with orthonormal columns and d[j] = |R_jj| of the
+    unpivoted QR factorisation b = Q R (m >= p). Q equals the Householder Q
+    of np.linalg.qr (mfg/kernels.py:94) up to column signs; d is what the
+    reference's |R_jj| <= tol ||b||_F screening reads."""
+    b = _mat(b)
+    m, p = b.shape
+    if p > m:
+        raise ValueError(f"qr: expected a tall block, got {m}x{p}")
+    q = torch.empty((m, p), dtype=torch.float64, device=b.device)
+    d = torch.empty((p,), dtype=torch.float64, device=b.device)
+    if p == 0:
+        return q, d
+    lib = _lib.lib()
+    wsb = int(lib.mfg_qr_workspace(m, p))
+    ws = _ws(wsb, b.device)
+    _lib.check(lib.mfg_qr(m, p, b.data_ptr(), p, q.data_ptr(), p, d.data_ptr(), ws.data_ptr(), wsb,
+                          _lib.stream_ptr()), "qr")
+    return q, d

@@ -40,8 +40,18 @@ def svd_from_factors(wf: FactorPair) -> SvdTriplet:
     """Compact SVD of W H^T via QR of the factors and a k x k SVD (35-45)."""
     if wf.k == 0:
         return SvdTriplet.zero(wf.m, wf.n)
-    qw, rw = torch.linalg.qr(wf.w.double())
-    qh, rh = torch.linalg.qr(wf.h.double())
+    from . import dense
+
+    def qr(a):
+        # our TSQR-panel QR (csrc/qr.cu); R = Q^T A on the DMMA Gram kernel
+        a = a.double()
+        if a.shape[1] > a.shape[0]:
+            return torch.linalg.qr(a)       # wide factor (test scale only)
+        q, _ = dense.qr(a)
+        return q, dense.gram(q, a)
+
+    qw, rw = qr(wf.w)
+    qh, rh = qr(wf.h)
     u_mid, s, vt_mid = torch.linalg.svd(rw @ rh.T)
     sh = s.cpu().numpy()
     if sh.size == 0 or sh[0] == 0.0:
