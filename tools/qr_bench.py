@@ -14,8 +14,12 @@ def t_ms(fn, reps=5):
     torch.cuda.synchronize()
     return (time.perf_counter() - t) / reps * 1e3, out
 
-for m, p in [(2000, 24), (2000, 96), (2000, 300), (1500, 300), (3706, 80), (6040, 320), (6040, 1600),
-             (10677, 240), (71567, 240), (17770, 160), (480189, 120)]:
+import sys
+SHAPES = [(2000, 24), (2000, 96), (2000, 300), (1500, 300), (3706, 80), (6040, 320), (6040, 1600),
+             (10677, 240), (71567, 240), (17770, 160), (480189, 120)]
+if len(sys.argv) > 1 and sys.argv[1] == "wide":
+    SHAPES = [(10677, 480), (10677, 960), (71567, 480), (71567, 960), (17770, 640), (6040, 800), (3706, 800), (2000, 600)]
+for m, p in SHAPES:
     b = torch.randn(m, p, dtype=torch.float64, device="cuda")
     b[:, : p // 4] *= 1e4
     ours, (q, d) = t_ms(lambda: dense.qr(b))
