@@ -1,6 +1,6 @@
 """Diagnostics: per-worker phase timing of the grouped sweep (globaltimer stamps)."""
 import sys, os, numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2204_14067_b200 import _lib, synth
 from paper_2204_14067_b200.data import ObservationSet
 from paper_2204_14067_b200.mfsolver import SweepPlan
