@@ -26,6 +26,7 @@ def timed(mod, name, label=None, shape_of=None):
 timed(K, "_householder", shape_of=lambda c: c.shape)
 timed(K, "_cholqr2", shape_of=lambda b, *r: b.shape)
 timed(K, "_scholqr3")
+timed(K, "_refactor_r", shape_of=lambda q, r, idx, j0: (r.shape[0], int(idx.numel()), j0))
 timed(torch.linalg, "eigh", "eigh", shape_of=lambda t, *r, **k: t.shape)
 timed(torch.linalg, "svd", "svd")
 timed(eigensolver, "_ritz")
@@ -52,6 +53,6 @@ torch.cuda.synchronize(); el = time.perf_counter() - t0
 print(f"{wl}: {len(trace) - 1} outer iterations, rank {x.rank}, {el:.2f} s (timers synchronise, so this is an upper bound)")
 for k_, t in T.most_common():
     print(f"  {k_:24s} {t:8.3f} s  {N[k_]:6d} calls  {1e3 * t / max(N[k_], 1):8.3f} ms/call")
-for lab in ("_householder", "_cholqr2", "eigh"):
+for lab in ("_householder", "_cholqr2", "_refactor_r", "eigh"):
     tops = sorted(((cnt, sh) for (l, sh), cnt in SH.items() if l == lab), reverse=True)[:8]
     print(f"  {lab} shapes (count, shape):", tops)
